@@ -1,0 +1,18 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA B200 (runs under gpurun / round-end GPU tier)")
+    config.addinivalue_line("markers", "slow: long-running (still part of the default suites)")
+
+
+@pytest.fixture(scope="session")
+def root():
+    return ROOT
