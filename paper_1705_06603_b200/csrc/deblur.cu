@@ -1,0 +1,1049 @@
+// deblur.cu -- libdeblur: C ABI (include/deblur.h), device state, orchestration.
+//
+// One handle = one rank = one GPU.  It owns the device copies of this rank's
+// facets (x ping/pong, u, v, y, w, r, g), the PSF taps and interpolation
+// weights, the tile / band work lists, the stream and (world > 1) the NCCL
+// communicator.  deblur_iterate runs Algorithm 1:
+//   per inner step: K1 (H + residual) -> K2 (H^T + TV + prox + projection)
+//   then: halo exchange of v = 2x+ - u over NCCL (world > 1)  -> K5 consensus.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/deblur.h"
+#include "fft.hpp"
+#include "kernels.hpp"
+#include "plan.hpp"
+
+using namespace deblur;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+enum KClass {
+    KC_H = 0, KC_HT_UPDATE, KC_CONSENSUS, KC_H_OBJ, KC_TV, KC_MAXDIFF, KC_XCHG, KC_HT_PLAIN, KC_H_PLAIN,
+    KC_FFT_H, KC_FFT_HT, KC_UPDATE_G, KC_COUNT
+};
+const char *k_names[KC_COUNT] = {"H_direct_residual", "HT_direct_update", "consensus", "H_direct_objective",
+                                 "tv_value", "maxdiff", "halo_exchange", "HT_direct_plain", "H_direct_plain",
+                                 "H_fft_residual", "HT_fft", "update_from_g"};
+
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+struct SendRecv {
+    Message m;
+    float *vbuf = nullptr;   // device buffer for v band
+    float *xbuf = nullptr;   // device buffer for x band (objective)
+};
+
+}  // namespace
+
+struct deblur_ctx {
+    deblur_params prm{};
+    Plan plan;
+    int rank = 0, world = 1, device = 0;
+    cudaStream_t stream = nullptr;
+    std::vector<int> local;               // facet ids owned by this rank (ascending)
+    std::vector<int> local_index;         // facet id -> local index or -1
+    std::vector<FacetDev> fh;             // host copies of the descriptors
+    FacetDev *d_facets = nullptr;
+    FacetDev *d_facets_alt = nullptr;     // x[] -> g (apply_H input)
+    std::vector<void *> allocs;
+    float *d_psfs = nullptr, *d_wy = nullptr, *d_wx = nullptr;
+    std::vector<TileDesc> tilesH, tilesHT;
+    TileDesc *d_tilesH = nullptr, *d_tilesHT = nullptr;
+    std::vector<BandRect> rects;
+    BandRect *d_rects = nullptr;
+    double *d_partials = nullptr;
+    std::vector<double> h_partials;
+    SolverConst sc{};
+    double tau = 0.0;
+    int par = 0;
+    int conv_path = DEBLUR_CONV_DIRECT;
+    FftPlan *fft = nullptr;
+    // host copies needed after create
+    std::vector<float> h_wy, h_wx;
+    // communication
+    ncclComm_t comm = nullptr;
+    std::vector<SendRecv> sends, recvs;
+    // instrumentation
+    bool prof = false;
+    struct Pending { int cls; cudaEvent_t a, b; };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> ev_pool;
+    int64_t stat_n[KC_COUNT] = {0};
+    double stat_ms[KC_COUNT] = {0};
+    // errors
+    std::string err;
+    bool poisoned = false;
+
+    deblur_status fail(deblur_status s, const std::string &m) {
+        err = m;
+        if (s == DEBLUR_ECUDA || s == DEBLUR_ENCCL) poisoned = true;
+        return s;
+    }
+    deblur_status cuda_fail(cudaError_t e, const char *what) {
+        std::ostringstream o;
+        o << "CUDA error " << cudaGetErrorName(e) << " (" << cudaGetErrorString(e) << ") in " << what;
+        return fail(DEBLUR_ECUDA, o.str());
+    }
+    deblur_status nccl_fail(ncclResult_t r, const char *phase, int peer) {
+        std::ostringstream o;
+        o << "NCCL error " << ncclGetErrorString(r) << " in " << phase;
+        if (peer >= 0) o << " (peer rank " << peer << ")";
+        return fail(DEBLUR_ENCCL, o.str());
+    }
+    template <typename T>
+    cudaError_t dalloc(T **p, size_t n) {
+        void *q = nullptr;
+        cudaError_t e = cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(T));
+        if (e == cudaSuccess) { allocs.push_back(q); *p = (T *)q; }
+        return e;
+    }
+    cudaEvent_t get_event() {
+        if (!ev_pool.empty()) { cudaEvent_t e = ev_pool.back(); ev_pool.pop_back(); return e; }
+        cudaEvent_t e; cudaEventCreate(&e); return e;
+    }
+    void prof_begin(int cls, cudaEvent_t *a) {
+        if (!prof) return;
+        *a = get_event();
+        cudaEventRecord(*a, stream);
+        (void)cls;
+    }
+    void prof_end(int cls, cudaEvent_t a) {
+        stat_n[cls] += 1;
+        if (!prof) return;
+        cudaEvent_t b = get_event();
+        cudaEventRecord(b, stream);
+        pending.push_back({cls, a, b});
+    }
+    void prof_collect() {
+        for (auto &p : pending) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) stat_ms[p.cls] += ms;
+            ev_pool.push_back(p.a);
+            ev_pool.push_back(p.b);
+        }
+        pending.clear();
+    }
+    ConvArgs conv_args(const FacetDev *facets, bool ht) const {
+        ConvArgs a;
+        a.facets = facets;
+        a.tiles = ht ? d_tilesHT : d_tilesH;
+        a.ntiles = (int)(ht ? tilesHT.size() : tilesH.size());
+        a.psfs = d_psfs; a.wy = d_wy; a.wx = d_wx;
+        a.P = plan.P; a.Gx = prm.psf_gx; a.Ny = (int)plan.ny; a.Nx = (int)plan.nx;
+        a.partials = d_partials;
+        return a;
+    }
+};
+
+#define CU(call)                                                      \
+    do {                                                              \
+        cudaError_t e_ = (call);                                      \
+        if (e_ != cudaSuccess) return h->cuda_fail(e_, #call);        \
+    } while (0)
+#define NC(call, phase, peer)                                         \
+    do {                                                              \
+        ncclResult_t r_ = (call);                                     \
+        if (r_ != ncclSuccess) return h->nccl_fail(r_, phase, peer);  \
+    } while (0)
+
+namespace {
+
+deblur_status validate(const deblur_params *p, std::string &err) {
+    std::ostringstream o;
+    if (!p) { err = "params is NULL"; return DEBLUR_EINVAL; }
+    if (p->abi_version != DEBLUR_ABI_VERSION) { o << "abi_version " << p->abi_version << " != " << DEBLUR_ABI_VERSION; err = o.str(); return DEBLUR_EINVAL; }
+    if (p->ny < 1 || p->nx < 1 || p->ny > (1 << 30) || p->nx > (1 << 30)) { err = "ny/nx out of range"; return DEBLUR_ESHAPE; }
+    if (p->psf_size < 1 || p->psf_size % 2 == 0) { err = "psf_size must be odd and >= 1"; return DEBLUR_EINVAL; }
+    if (p->psf_size > p->ny || p->psf_size > p->nx) { err = "psf_size larger than the image"; return DEBLUR_ESHAPE; }
+    if (p->psf_gy < 1 || p->psf_gx < 1) { err = "psf_gy/psf_gx must be >= 1"; return DEBLUR_EINVAL; }
+    if (!p->psfs) { err = "psfs is NULL"; return DEBLUR_EINVAL; }
+    if (!p->interp_wy || !p->interp_wx) { err = "interp_wy/interp_wx is NULL"; return DEBLUR_EINVAL; }
+    if (!p->y) { err = "y is NULL"; return DEBLUR_EINVAL; }
+    if (!p->noise_w && !(p->noise_w_scalar >= 0.f)) { err = "noise_w_scalar must be >= 0"; return DEBLUR_EINVAL; }
+    if (!(p->lambda >= 0.f)) { err = "lambda must be >= 0"; return DEBLUR_EINVAL; }
+    if (!(p->eps > 0.f)) { err = "eps must be > 0"; return DEBLUR_EINVAL; }
+    if (p->reg_kind != 0 && p->reg_kind != 1) { err = "reg_kind must be 0 or 1"; return DEBLUR_EINVAL; }
+    if (p->tv_boundary != 0 && p->tv_boundary != 1) { err = "tv_boundary must be 0 or 1"; return DEBLUR_EINVAL; }
+    if (!(p->gamma >= 0.f)) { err = "gamma must be >= 0"; return DEBLUR_EINVAL; }
+    if (!(p->rho > 0.f && p->rho < 2.f)) { err = "rho must be in (0, 2) (PAPER.md:147)"; return DEBLUR_EINVAL; }
+    if (p->inner_steps < 1) { err = "inner_steps must be >= 1"; return DEBLUR_EINVAL; }
+    if (p->facet_gy < 1 || p->facet_gx < 1) { err = "facet_gy/facet_gx must be >= 1"; return DEBLUR_EINVAL; }
+    if (p->overlap < 0 || p->overlap % 2) { err = "overlap must be even and >= 0"; return DEBLUR_EINVAL; }
+    if (p->conv_path < 0 || p->conv_path > 2) { err = "conv_path must be 0, 1 or 2"; return DEBLUR_EINVAL; }
+    if (p->world < 1 || p->rank < 0 || p->rank >= p->world) { err = "rank/world out of range"; return DEBLUR_EINVAL; }
+    if (p->world > 1 && !p->nccl_id) { err = "nccl_id is NULL with world > 1"; return DEBLUR_EINVAL; }
+    if (!(std::isfinite(p->tau))) { err = "tau must be finite"; return DEBLUR_EINVAL; }
+    return DEBLUR_OK;
+}
+
+// A4': tau = 1/L, L = max(w) S^2 a_row a_col + lambda * 8 * Lip(psi) + gamma
+double default_tau(const deblur_params *p) {
+    const int P = p->psf_size, K = p->psf_gy * p->psf_gx;
+    const int64_t my = p->ny - P + 1, mx = p->nx - P + 1;
+    double sy = 0, sx = 0;
+    for (int64_t r = 0; r < p->ny; ++r) {
+        double s = 0;
+        for (int k = 0; k < p->psf_gy; ++k) s += std::fabs((double)p->interp_wy[(int64_t)k * p->ny + r]);
+        sy = std::max(sy, s);
+    }
+    for (int64_t c = 0; c < p->nx; ++c) {
+        double s = 0;
+        for (int k = 0; k < p->psf_gx; ++k) s += std::fabs((double)p->interp_wx[(int64_t)k * p->nx + c]);
+        sx = std::max(sx, s);
+    }
+    const double S = sy * sx;
+    double a_row = 0, a_col = 0;
+    for (int i = 0; i < P * P; ++i) {
+        double m = 0;
+        for (int k = 0; k < K; ++k) m = std::max(m, std::fabs((double)p->psfs[(int64_t)k * P * P + i]));
+        a_row += m;
+    }
+    for (int k = 0; k < K; ++k) {
+        double s = 0;
+        for (int i = 0; i < P * P; ++i) s += std::fabs((double)p->psfs[(int64_t)k * P * P + i]);
+        a_col = std::max(a_col, s);
+    }
+    double wmax = 0;
+    if (p->noise_w) {
+        for (int64_t i = 0; i < my * mx; ++i) wmax = std::max(wmax, (double)p->noise_w[i]);
+    } else {
+        wmax = (double)p->noise_w_scalar;
+    }
+    const double lip = (p->reg_kind == 0) ? 1.0 / (double)p->eps : 1.0;
+    const double L = wmax * S * S * a_row * a_col + (double)p->lambda * 8.0 * lip + (double)p->gamma;
+    return L > 0 ? 1.0 / L : 1.0;
+}
+
+// Active PSF index range [lo, hi] whose weight row is nonzero somewhere on [a, b).
+struct NzIndex {
+    int G = 0; int64_t n = 0;
+    std::vector<int64_t> pre;   // [G][n+1] prefix counts of nonzeros
+    void build(const float *w, int G_, int64_t n_) {
+        G = G_; n = n_;
+        pre.assign((size_t)G * (n + 1), 0);
+        for (int g = 0; g < G; ++g)
+            for (int64_t i = 0; i < n; ++i)
+                pre[(size_t)g * (n + 1) + i + 1] = pre[(size_t)g * (n + 1) + i] + (w[(size_t)g * n + i] != 0.f);
+    }
+    void range(int64_t a, int64_t b, int &lo, int &hi) const {
+        a = std::max<int64_t>(0, a); b = std::min<int64_t>(n, b);
+        lo = G; hi = -1;
+        if (a >= b) return;
+        for (int g = 0; g < G; ++g) {
+            if (pre[(size_t)g * (n + 1) + b] - pre[(size_t)g * (n + 1) + a] > 0) { lo = std::min(lo, g); hi = std::max(hi, g); }
+        }
+    }
+};
+
+}  // namespace
+
+// ----------------------------------------------------------------------------- helpers
+static deblur_status upload_slice(deblur_t h, float *dst, int64_t dpitch, const float *src, int64_t spitch,
+                                  int64_t y0, int64_t x0, int64_t rows, int64_t cols) {
+    CU(cudaMemcpy2DAsync(dst, dpitch * 4, src + y0 * spitch + x0, spitch * 4, cols * 4, rows,
+                         cudaMemcpyHostToDevice, h->stream));
+    return DEBLUR_OK;
+}
+
+static std::vector<float> default_x0(const deblur_params *p) {
+    // A6: x0 = u0 = max(0, y edge-replicated into the c-wide margin)
+    const int c = (p->psf_size - 1) / 2;
+    const int64_t my = p->ny - p->psf_size + 1, mx = p->nx - p->psf_size + 1;
+    std::vector<float> x((size_t)(p->ny * p->nx));
+    for (int64_t r = 0; r < p->ny; ++r) {
+        const int64_t yr = std::min<int64_t>(std::max<int64_t>(r - c, 0), my - 1);
+        for (int64_t q = 0; q < p->nx; ++q) {
+            const int64_t yq = std::min<int64_t>(std::max<int64_t>(q - c, 0), mx - 1);
+            x[(size_t)(r * p->nx + q)] = std::max(0.f, p->y[yr * mx + yq]);
+        }
+    }
+    return x;
+}
+
+static deblur_status upload_state_x0(deblur_t h, const float *x0) {
+    std::vector<float> tmp;
+    if (!x0) { tmp = default_x0(&h->prm); x0 = tmp.data(); }
+    for (size_t li = 0; li < h->local.size(); ++li) {
+        const FacetPlan &fp = h->plan.facets[h->local[li]];
+        FacetDev &F = h->fh[li];
+        deblur_status s;
+        if ((s = upload_slice(h, F.x[0], F.ep, x0, h->plan.nx, fp.ey0, fp.ex0, F.ny, F.nx)) != DEBLUR_OK) return s;
+        if ((s = upload_slice(h, F.u, F.ep, x0, h->plan.nx, fp.ey0, fp.ex0, F.ny, F.nx)) != DEBLUR_OK) return s;
+    }
+    h->par = 0;
+    CU(cudaStreamSynchronize(h->stream));
+    return DEBLUR_OK;
+}
+
+static deblur_status upload_y(deblur_t h, const float *y) {
+    for (size_t li = 0; li < h->local.size(); ++li) {
+        const FacetPlan &fp = h->plan.facets[h->local[li]];
+        FacetDev &F = h->fh[li];
+        deblur_status s = upload_slice(h, (float *)F.y, F.op, y, h->plan.mx, fp.oy0, fp.ox0, F.my, F.mx);
+        if (s != DEBLUR_OK) return s;
+    }
+    return DEBLUR_OK;
+}
+
+static deblur_status check_state(deblur_t h) {
+    if (!h) return DEBLUR_EINVAL;
+    if (h->poisoned) { return DEBLUR_ESTATE; }
+    cudaError_t e = cudaSetDevice(h->device);
+    if (e != cudaSuccess) return h->cuda_fail(e, "cudaSetDevice");
+    return DEBLUR_OK;
+}
+
+// halo exchange: v bands (which == 0) or x[par] bands (which == 1)
+static deblur_status exchange(deblur_t h, int which) {
+    if (h->world == 1 || (h->sends.empty() && h->recvs.empty())) return DEBLUR_OK;
+    cudaEvent_t ev = nullptr;
+    h->prof_begin(KC_XCHG, &ev);
+    for (auto &s : h->sends) {
+        const FacetDev &F = h->fh[h->local_index[s.m.src_facet]];
+        const float *src = which == 0 ? F.v : F.x[h->par];
+        const int64_t w = s.m.rect.x1 - s.m.rect.x0, hh = s.m.rect.y1 - s.m.rect.y0;
+        const float *p = src + (s.m.rect.y0 - F.ey0) * F.ep + (s.m.rect.x0 - F.ex0);
+        CU(cudaMemcpy2DAsync(which == 0 ? s.vbuf : s.xbuf, w * 4, p, F.ep * 4, w * 4, hh, cudaMemcpyDeviceToDevice,
+                             h->stream));
+    }
+    NC(ncclGroupStart(), "halo group start", -1);
+    for (auto &s : h->sends)
+        NC(ncclSend(which == 0 ? s.vbuf : s.xbuf, (size_t)s.m.rect.area(), ncclFloat, s.m.peer, h->comm, h->stream),
+           "halo send", s.m.peer);
+    for (auto &r : h->recvs)
+        NC(ncclRecv(which == 0 ? r.vbuf : r.xbuf, (size_t)r.m.rect.area(), ncclFloat, r.m.peer, h->comm, h->stream),
+           "halo recv", r.m.peer);
+    NC(ncclGroupEnd(), "halo group end", -1);
+    h->prof_end(KC_XCHG, ev);
+    return DEBLUR_OK;
+}
+
+static deblur_status finish(deblur_t h) {
+    CU(cudaStreamSynchronize(h->stream));
+    CU(cudaGetLastError());
+    if (h->comm) {
+        ncclResult_t ar;
+        if (ncclCommGetAsyncError(h->comm, &ar) == ncclSuccess && ar != ncclSuccess)
+            return h->nccl_fail(ar, "async", -1);
+    }
+    h->prof_collect();
+    return DEBLUR_OK;
+}
+
+// One Local-Solver step on every local facet (K1 + K2, or the FFT path + K4).
+static deblur_status local_step(deblur_t h, int last) {
+    cudaEvent_t ev = nullptr;
+    if (h->conv_path == DEBLUR_CONV_FFT) {
+        h->prof_begin(KC_FFT_H, &ev);
+        CU(fft_H(*h->fft, h->d_facets, h->par, FFT_RESIDUAL, h->stream));
+        h->prof_end(KC_FFT_H, ev);
+        h->prof_begin(KC_FFT_HT, &ev);
+        CU(fft_HT(*h->fft, h->d_facets, h->stream));
+        h->prof_end(KC_FFT_HT, ev);
+        h->prof_begin(KC_UPDATE_G, &ev);
+        CU(launch_update_from_g(h->d_facets, h->d_tilesHT, (int)h->tilesHT.size(), h->plan.P, h->par, last, h->sc,
+                                h->d_partials, h->stream));
+        h->prof_end(KC_UPDATE_G, ev);
+    } else {
+        h->prof_begin(KC_H, &ev);
+        CU(launch_H_direct(h->conv_args(h->d_facets, false), H_RESIDUAL, h->par, h->stream));
+        h->prof_end(KC_H, ev);
+        h->prof_begin(KC_HT_UPDATE, &ev);
+        CU(launch_HT_direct(h->conv_args(h->d_facets, true), HT_UPDATE, h->par, last, h->sc, h->stream));
+        h->prof_end(KC_HT_UPDATE, ev);
+    }
+    h->par ^= 1;
+    return DEBLUR_OK;
+}
+
+// ----------------------------------------------------------------------------- C ABI
+extern "C" {
+
+deblur_status deblur_nccl_id(void *out128) {
+    if (!out128) return DEBLUR_EINVAL;
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) { g_last_error = std::string("ncclGetUniqueId: ") + ncclGetErrorString(r); return DEBLUR_ENCCL; }
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(out128, &id, 128);
+    return DEBLUR_OK;
+}
+
+const char *deblur_last_error(deblur_t h) { return h ? h->err.c_str() : g_last_error.c_str(); }
+
+const char *deblur_kernel_name(int32_t cls) { return (cls >= 0 && cls < KC_COUNT) ? k_names[cls] : ""; }
+
+deblur_status deblur_plan_facets(const deblur_params *p, int32_t *n_facets, int64_t *boxes, int32_t *owner) {
+    std::string err;
+    deblur_status s = validate(p, err);
+    if (s != DEBLUR_OK) { g_last_error = err; return s; }
+    Plan pl;
+    err = make_plan(p->ny, p->nx, p->psf_size, p->facet_gy, p->facet_gx, p->overlap, p->world, pl);
+    if (!err.empty()) { g_last_error = err; return DEBLUR_ESHAPE; }
+    if (n_facets) *n_facets = (int32_t)pl.facets.size();
+    for (size_t i = 0; i < pl.facets.size(); ++i) {
+        const FacetPlan &f = pl.facets[i];
+        if (boxes) {
+            const int64_t b[8] = {f.oy0, f.oy1, f.ox0, f.ox1, f.ey0, f.ey1, f.ex0, f.ex1};
+            std::memcpy(boxes + 8 * i, b, sizeof b);
+        }
+        if (owner) owner[i] = f.owner;
+    }
+    return DEBLUR_OK;
+}
+
+deblur_status deblur_plan_messages(const deblur_params *p, int32_t rank, int32_t *n, int64_t *msgs) {
+    std::string err;
+    deblur_status s = validate(p, err);
+    if (s != DEBLUR_OK) { g_last_error = err; return s; }
+    if (!n) { g_last_error = "n is NULL"; return DEBLUR_EINVAL; }
+    Plan pl;
+    err = make_plan(p->ny, p->nx, p->psf_size, p->facet_gy, p->facet_gx, p->overlap, p->world, pl);
+    if (!err.empty()) { g_last_error = err; return DEBLUR_ESHAPE; }
+    if (rank < 0 || rank >= p->world) { g_last_error = "rank out of range"; return DEBLUR_EINVAL; }
+    auto m = messages_from(pl, rank);
+    *n = (int32_t)m.size();
+    if (msgs)
+        for (size_t i = 0; i < m.size(); ++i) {
+            const int64_t r[8] = {m[i].peer, m[i].src_facet, m[i].dst_facet, m[i].rect.y0, m[i].rect.y1,
+                                  m[i].rect.x0, m[i].rect.x1, m[i].bytes()};
+            std::memcpy(msgs + 8 * i, r, sizeof r);
+        }
+    return DEBLUR_OK;
+}
+
+deblur_status deblur_destroy(deblur_t h) {
+    if (!h) return DEBLUR_OK;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->fft) { fft_destroy(h->fft); h->fft = nullptr; }
+    if (h->comm) { ncclCommDestroy(h->comm); h->comm = nullptr; }
+    for (auto &p : h->pending) { h->ev_pool.push_back(p.a); h->ev_pool.push_back(p.b); }
+    for (auto e : h->ev_pool) cudaEventDestroy(e);
+    for (void *p : h->allocs) cudaFree(p);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+    return DEBLUR_OK;
+}
+
+deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
+    if (!out) { g_last_error = "out is NULL"; return DEBLUR_EINVAL; }
+    *out = nullptr;
+    std::string err;
+    deblur_status st = validate(p, err);
+    if (st != DEBLUR_OK) { g_last_error = err; return st; }
+    std::unique_ptr<deblur_ctx> hp(new (std::nothrow) deblur_ctx());
+    if (!hp) { g_last_error = "host allocation failed"; return DEBLUR_ENOMEM; }
+    deblur_t h = hp.get();
+    h->prm = *p;
+    h->rank = p->rank; h->world = p->world; h->device = p->device;
+    err = make_plan(p->ny, p->nx, p->psf_size, p->facet_gy, p->facet_gx, p->overlap, p->world, h->plan);
+    if (!err.empty()) { g_last_error = err; return DEBLUR_ESHAPE; }
+    const Plan &pl = h->plan;
+    const int P = pl.P;
+
+    // device
+    int ndev = 0;
+    cudaError_t ce = cudaGetDeviceCount(&ndev);
+    if (ce != cudaSuccess || ndev == 0) {
+        g_last_error = std::string("no CUDA device: ") + (ce != cudaSuccess ? cudaGetErrorString(ce) : "count 0");
+        return DEBLUR_ECUDA;
+    }
+    if (p->device < 0 || p->device >= ndev) { g_last_error = "device ordinal out of range"; return DEBLUR_EINVAL; }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, p->device) != cudaSuccess || prop.major != 10) {
+        g_last_error = "device is not sm_100 (this library is built for sm_100a only; no fallback)";
+        return DEBLUR_ECUDA;
+    }
+#define CUC(call)                                                                             \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess) {                                                              \
+            g_last_error = std::string("CUDA error in create: ") + cudaGetErrorString(e_) + " at " #call; \
+            return e_ == cudaErrorMemoryAllocation ? DEBLUR_ENOMEM : DEBLUR_ECUDA;             \
+        }                                                                                     \
+    } while (0)
+    CUC(cudaSetDevice(p->device));
+    CUC(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+
+    // conv path (A: measured crossover)
+    int path = p->conv_path;
+    if (path == DEBLUR_CONV_AUTO) path = fft_prefer(P) ? DEBLUR_CONV_FFT : DEBLUR_CONV_DIRECT;
+    if (path == DEBLUR_CONV_DIRECT && !direct_supported(P)) {
+        g_last_error = "psf_size too large for the direct path; use conv_path FFT";
+        return DEBLUR_EINVAL;
+    }
+    h->conv_path = path;
+
+    // global read-only inputs
+    const int K = p->psf_gy * p->psf_gx;
+    CUC(h->dalloc(&h->d_psfs, (size_t)K * P * P));
+    CUC(h->dalloc(&h->d_wy, (size_t)p->psf_gy * p->ny));
+    CUC(h->dalloc(&h->d_wx, (size_t)p->psf_gx * p->nx));
+    CUC(cudaMemcpy(h->d_psfs, p->psfs, sizeof(float) * K * P * P, cudaMemcpyHostToDevice));
+    CUC(cudaMemcpy(h->d_wy, p->interp_wy, sizeof(float) * p->psf_gy * p->ny, cudaMemcpyHostToDevice));
+    CUC(cudaMemcpy(h->d_wx, p->interp_wx, sizeof(float) * p->psf_gx * p->nx, cudaMemcpyHostToDevice));
+    h->h_wy.assign(p->interp_wy, p->interp_wy + (size_t)p->psf_gy * p->ny);
+    h->h_wx.assign(p->interp_wx, p->interp_wx + (size_t)p->psf_gx * p->nx);
+
+    // local facets
+    h->local_index.assign(pl.facets.size(), -1);
+    for (const auto &f : pl.facets)
+        if (f.owner == h->rank) { h->local_index[f.id] = (int)h->local.size(); h->local.push_back(f.id); }
+    auto axisw = [](int64_t e0, int64_t e1, int64_t pe, int64_t ns) {
+        AxisW a;
+        a.e0 = (int)e0; a.n = (int)(e1 - e0);
+        a.b_prev = (int)(pe - e0); a.b_next = (int)(ns - e0);
+        a.s_prev = (int)e0; a.e_prev = (int)pe;
+        a.s_next = (int)ns; a.e_next = (int)e1;
+        return a;
+    };
+    for (int id : h->local) {
+        const FacetPlan &fp = pl.facets[id];
+        FacetDev F{};
+        F.id = id;
+        F.ny = (int)(fp.ey1 - fp.ey0); F.nx = (int)(fp.ex1 - fp.ex0);
+        F.my = (int)(fp.oy1 - fp.oy0); F.mx = (int)(fp.ox1 - fp.ox0);
+        F.ey0 = (int)fp.ey0; F.ex0 = (int)fp.ex0;
+        F.ep = round_up(F.nx, 32); F.op = round_up(F.mx, 32);
+        const size_t ne = (size_t)F.ny * F.ep, no = (size_t)F.my * F.op;
+        float *y_ = nullptr, *w_ = nullptr;
+        CUC(h->dalloc(&F.x[0], ne)); CUC(h->dalloc(&F.x[1], ne));
+        CUC(h->dalloc(&F.u, ne)); CUC(h->dalloc(&F.v, ne)); CUC(h->dalloc(&F.g, ne));
+        CUC(h->dalloc(&y_, no)); CUC(h->dalloc(&F.r, no));
+        for (float *b : {F.x[0], F.x[1], F.u, F.v, F.g}) CUC(cudaMemsetAsync(b, 0, ne * 4, h->stream));
+        CUC(cudaMemsetAsync(y_, 0, no * 4, h->stream)); CUC(cudaMemsetAsync(F.r, 0, no * 4, h->stream));
+        if (p->noise_w) {
+            CUC(h->dalloc(&w_, no));
+            CUC(cudaMemsetAsync(w_, 0, no * 4, h->stream));
+            CUC(cudaMemcpy2DAsync(w_, F.op * 4, p->noise_w + fp.oy0 * pl.mx + fp.ox0, pl.mx * 4, F.mx * 4, F.my,
+                                  cudaMemcpyHostToDevice, h->stream));
+        }
+        F.y = y_; F.w = w_; F.w_scalar = p->noise_w_scalar;
+        F.ay = axisw(fp.ey0, fp.ey1, fp.py_e, fp.ny_s);
+        F.ax = axisw(fp.ex0, fp.ex1, fp.px_e, fp.nx_s);
+        for (int dy = 0; dy < 3; ++dy)
+            for (int dx = 0; dx < 3; ++dx) F.nb[dy][dx].id = -1;
+        h->fh.push_back(F);
+    }
+
+    // halo messages (world > 1) and neighbour views
+    h->sends.clear(); h->recvs.clear();
+    if (h->world > 1) {
+        for (auto &m : messages_from(pl, h->rank)) { SendRecv s; s.m = m; h->sends.push_back(s); }
+        for (auto &m : messages_to(pl, h->rank)) { SendRecv s; s.m = m; h->recvs.push_back(s); }
+        for (auto *lst : {&h->sends, &h->recvs})
+            for (auto &s : *lst) {
+                CUC(h->dalloc(&s.vbuf, (size_t)s.m.rect.area()));
+                CUC(h->dalloc(&s.xbuf, (size_t)s.m.rect.area()));
+            }
+    }
+    for (size_t li = 0; li < h->local.size(); ++li) {
+        FacetDev &F = h->fh[li];
+        const FacetPlan &fp = pl.facets[F.id];
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int gy = fp.fy + dy, gx = fp.fx + dx;
+                if (gy < 0 || gy >= pl.Fy || gx < 0 || gx >= pl.Fx) continue;
+                const FacetPlan &np = pl.facets[gy * pl.Fx + gx];
+                Neighbour &nb = F.nb[dy + 1][dx + 1];
+                nb.id = np.id;
+                nb.ay = axisw(np.ey0, np.ey1, np.py_e, np.ny_s);
+                nb.ax = axisw(np.ex0, np.ex1, np.px_e, np.nx_s);
+                const int nli = h->local_index[np.id];
+                if (nli >= 0) {
+                    const FacetDev &N = (nli == (int)li) ? F : h->fh[nli];
+                    nb.v.base[0] = nb.v.base[1] = N.v;
+                    nb.v.pitch = N.ep; nb.v.y0 = N.ey0; nb.v.x0 = N.ex0; nb.v.valid = 1;
+                    nb.x.base[0] = N.x[0]; nb.x.base[1] = N.x[1];
+                    nb.x.pitch = N.ep; nb.x.y0 = N.ey0; nb.x.x0 = N.ex0; nb.x.valid = 1;
+                } else {
+                    for (auto &r : h->recvs)
+                        if (r.m.src_facet == np.id && r.m.dst_facet == F.id) {
+                            const int64_t w = r.m.rect.x1 - r.m.rect.x0;
+                            nb.v.base[0] = nb.v.base[1] = r.vbuf;
+                            nb.v.pitch = w; nb.v.y0 = (int)r.m.rect.y0; nb.v.x0 = (int)r.m.rect.x0; nb.v.valid = 1;
+                            nb.x.base[0] = nb.x.base[1] = r.xbuf;
+                            nb.x.pitch = w; nb.x.y0 = (int)r.m.rect.y0; nb.x.x0 = (int)r.m.rect.x0; nb.x.valid = 1;
+                        }
+                }
+            }
+        // band rectangles (facet-local): pixels in >= 2 facets
+        const int by0 = F.ay.b_prev, by1 = F.ay.b_next, bx0 = F.ax.b_prev, bx1 = F.ax.b_next;
+        auto add = [&](int y0, int y1, int x0, int x1) {
+            if (y1 > y0 && x1 > x0) h->rects.push_back({(int)li, y0, y1, x0, x1});
+        };
+        add(0, by0, 0, F.nx);
+        add(by1, F.ny, 0, F.nx);
+        add(by0, by1, 0, bx0);
+        add(by0, by1, bx1, F.nx);
+    }
+
+    // tiles with active PSF ranges
+    NzIndex nzy, nzx;
+    nzy.build(p->interp_wy, p->psf_gy, p->ny);
+    nzx.build(p->interp_wx, p->psf_gx, p->nx);
+    const int tyH = direct_ty_H(P), tyHT = direct_ty_HT(P), TXd = DIRECT_TX;
+    for (size_t li = 0; li < h->local.size(); ++li) {
+        const FacetDev &F = h->fh[li];
+        for (int y0 = 0; y0 < F.my; y0 += tyH)
+            for (int x0 = 0; x0 < F.mx; x0 += TXd) {
+                TileDesc t{(int)li, y0, x0, 0, -1, 0, -1};
+                nzy.range(F.ey0 + y0, F.ey0 + std::min(y0 + tyH + P - 1, F.ny), t.p0, t.p1);
+                nzx.range(F.ex0 + x0, F.ex0 + std::min(x0 + TXd + P - 1, F.nx), t.q0, t.q1);
+                h->tilesH.push_back(t);
+            }
+        for (int y0 = 0; y0 < F.ny; y0 += tyHT)
+            for (int x0 = 0; x0 < F.nx; x0 += TXd) {
+                TileDesc t{(int)li, y0, x0, 0, -1, 0, -1};
+                nzy.range(F.ey0 + y0, F.ey0 + std::min(y0 + tyHT, F.ny), t.p0, t.p1);
+                nzx.range(F.ex0 + x0, F.ex0 + std::min(x0 + TXd, F.nx), t.q0, t.q1);
+                h->tilesHT.push_back(t);
+            }
+    }
+    CUC(h->dalloc(&h->d_tilesH, h->tilesH.size()));
+    CUC(h->dalloc(&h->d_tilesHT, h->tilesHT.size()));
+    CUC(h->dalloc(&h->d_rects, h->rects.size()));
+    CUC(cudaMemcpy(h->d_tilesH, h->tilesH.data(), sizeof(TileDesc) * h->tilesH.size(), cudaMemcpyHostToDevice));
+    CUC(cudaMemcpy(h->d_tilesHT, h->tilesHT.data(), sizeof(TileDesc) * h->tilesHT.size(), cudaMemcpyHostToDevice));
+    CUC(cudaMemcpy(h->d_rects, h->rects.data(), sizeof(BandRect) * h->rects.size(), cudaMemcpyHostToDevice));
+    const size_t npart = std::max({h->tilesH.size(), h->tilesHT.size(), h->rects.size(), (size_t)1});
+    CUC(h->dalloc(&h->d_partials, npart));
+    h->h_partials.resize(npart);
+
+    CUC(h->dalloc(&h->d_facets, h->fh.size()));
+    CUC(h->dalloc(&h->d_facets_alt, h->fh.size()));
+    CUC(cudaMemcpy(h->d_facets, h->fh.data(), sizeof(FacetDev) * h->fh.size(), cudaMemcpyHostToDevice));
+    {
+        std::vector<FacetDev> alt = h->fh;
+        for (auto &F : alt) { F.x[0] = F.x[1] = F.g; }
+        CUC(cudaMemcpy(h->d_facets_alt, alt.data(), sizeof(FacetDev) * alt.size(), cudaMemcpyHostToDevice));
+    }
+
+    // solver constants
+    h->tau = (p->tau > 0) ? p->tau : default_tau(p);
+    h->sc.lambda = p->lambda; h->sc.eps = p->eps; h->sc.gamma = p->gamma; h->sc.rho = p->rho;
+    h->sc.tau = (float)h->tau; h->sc.reg_kind = p->reg_kind; h->sc.tv_boundary = p->tv_boundary;
+
+    // data + initial state
+    st = upload_y(h, p->y);
+    if (st != DEBLUR_OK) { g_last_error = h->err; return st; }
+    st = upload_state_x0(h, p->x0);
+    if (st != DEBLUR_OK) { g_last_error = h->err; return st; }
+
+    // FFT path plan
+    if (h->conv_path == DEBLUR_CONV_FFT) {
+        std::string ferr;
+        h->fft = fft_create(pl, h->local, h->fh, h->d_psfs, h->d_wy, h->d_wx, p->psf_gy, p->psf_gx, h->h_wy.data(),
+                            h->h_wx.data(), h->stream, ferr);
+        if (!h->fft) { g_last_error = "FFT path: " + ferr; return DEBLUR_ECUDA; }
+    }
+
+    // NCCL
+    if (h->world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, p->nccl_id, sizeof id);
+        ncclResult_t r = ncclCommInitRank(&h->comm, h->world, id, h->rank);
+        if (r != ncclSuccess) { g_last_error = std::string("ncclCommInitRank: ") + ncclGetErrorString(r); return DEBLUR_ENCCL; }
+    }
+    CUC(cudaStreamSynchronize(h->stream));
+    h->prm.psfs = nullptr; h->prm.interp_wy = h->prm.interp_wx = nullptr;
+    h->prm.y = h->prm.noise_w = h->prm.x0 = nullptr; h->prm.nccl_id = nullptr;
+    *out = hp.release();
+#undef CUC
+    return DEBLUR_OK;
+}
+
+deblur_status deblur_iterate(deblur_t h, int32_t n) {
+    deblur_status s = check_state(h);
+    if (s != DEBLUR_OK) return s;
+    if (n < 0) return h->fail(DEBLUR_EINVAL, "n must be >= 0");
+    for (int it = 0; it < n; ++it) {
+        for (int k = 0; k < h->prm.inner_steps; ++k)
+            if ((s = local_step(h, k == h->prm.inner_steps - 1)) != DEBLUR_OK) return s;
+        if ((s = exchange(h, 0)) != DEBLUR_OK) return s;
+        cudaEvent_t ev = nullptr;
+        h->prof_begin(KC_CONSENSUS, &ev);
+        CU(launch_consensus(h->d_facets, h->d_rects, (int)h->rects.size(), h->par, h->sc.rho, h->stream));
+        h->prof_end(KC_CONSENSUS, ev);
+    }
+    return finish(h);
+}
+
+deblur_status deblur_objective(deblur_t h, double out[4]) {
+    deblur_status s = check_state(h);
+    if (s != DEBLUR_OK) return s;
+    if (!out) return h->fail(DEBLUR_EINVAL, "out is NULL");
+    const int F = (int)h->plan.facets.size();
+    std::vector<double> data(F, 0.0), reg(F, 0.0);
+    double md = 0.0;
+    cudaEvent_t ev = nullptr;
+    // data term at the current x (A22)
+    if (h->conv_path == DEBLUR_CONV_FFT) {
+        h->prof_begin(KC_FFT_H, &ev);
+        CU(fft_H(*h->fft, h->d_facets, h->par, FFT_OBJECTIVE, h->stream));
+        h->prof_end(KC_FFT_H, ev);
+        CU(cudaStreamSynchronize(h->stream));
+        std::vector<double> fd;
+        CU(fft_data_partials(*h->fft, fd));
+        for (size_t li = 0; li < h->local.size(); ++li) data[h->local[li]] = fd[li];
+    } else {
+        h->prof_begin(KC_H_OBJ, &ev);
+        CU(launch_H_direct(h->conv_args(h->d_facets, false), H_OBJECTIVE, h->par, h->stream));
+        h->prof_end(KC_H_OBJ, ev);
+        CU(cudaMemcpyAsync(h->h_partials.data(), h->d_partials, sizeof(double) * h->tilesH.size(),
+                           cudaMemcpyDeviceToHost, h->stream));
+        CU(cudaStreamSynchronize(h->stream));
+        for (size_t t = 0; t < h->tilesH.size(); ++t) data[h->local[h->tilesH[t].f]] += h->h_partials[t];
+    }
+    h->prof_begin(KC_TV, &ev);
+    CU(launch_tv_value(h->d_facets, h->d_tilesHT, (int)h->tilesHT.size(), h->plan.P, h->par, h->sc, h->d_partials,
+                       h->stream));
+    h->prof_end(KC_TV, ev);
+    CU(cudaMemcpyAsync(h->h_partials.data(), h->d_partials, sizeof(double) * h->tilesHT.size(), cudaMemcpyDeviceToHost,
+                       h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    for (size_t t = 0; t < h->tilesHT.size(); ++t) reg[h->local[h->tilesHT[t].f]] += h->h_partials[t];
+    if ((s = exchange(h, 1)) != DEBLUR_OK) return s;
+    h->prof_begin(KC_MAXDIFF, &ev);
+    CU(launch_maxdiff(h->d_facets, h->d_rects, (int)h->rects.size(), h->par, h->d_partials, h->stream));
+    h->prof_end(KC_MAXDIFF, ev);
+    CU(cudaMemcpyAsync(h->h_partials.data(), h->d_partials, sizeof(double) * h->rects.size(), cudaMemcpyDeviceToHost,
+                       h->stream));
+    if ((s = finish(h)) != DEBLUR_OK) return s;
+    for (size_t r = 0; r < h->rects.size(); ++r) md = std::max(md, h->h_partials[r]);
+    if (h->world > 1) {
+        // per-facet values are nonzero only on their owner: a sum all-reduce is exact
+        double *d = nullptr;
+        CU(h->dalloc(&d, 2 * F + 1));
+        std::vector<double> buf(2 * F + 1);
+        for (int f = 0; f < F; ++f) { buf[f] = data[f]; buf[F + f] = reg[f]; }
+        buf[2 * F] = md;
+        CU(cudaMemcpy(d, buf.data(), sizeof(double) * (2 * F + 1), cudaMemcpyHostToDevice));
+        NC(ncclAllReduce(d, d, 2 * F, ncclDouble, ncclSum, h->comm, h->stream), "objective allreduce", -1);
+        NC(ncclAllReduce(d + 2 * F, d + 2 * F, 1, ncclDouble, ncclMax, h->comm, h->stream), "objective allreduce", -1);
+        CU(cudaMemcpyAsync(buf.data(), d, sizeof(double) * (2 * F + 1), cudaMemcpyDeviceToHost, h->stream));
+        CU(cudaStreamSynchronize(h->stream));
+        for (int f = 0; f < F; ++f) { data[f] = buf[f]; reg[f] = buf[F + f]; }
+        md = buf[2 * F];
+    }
+    double dt = 0, rt = 0;
+    for (int f = 0; f < F; ++f) {      // facet-id order
+        if (!std::isfinite(data[f]) || !std::isfinite(reg[f])) {
+            std::ostringstream o;
+            o << "non-finite objective partial on facet " << f;
+            return h->fail(DEBLUR_ENUMERIC, o.str());
+        }
+        dt += data[f];
+        rt += (double)h->prm.lambda * reg[f];
+    }
+    out[0] = dt + rt; out[1] = dt; out[2] = rt; out[3] = md;
+    return DEBLUR_OK;
+}
+
+}  // extern "C"
+
+// gather facet-local rectangles to rank 0's host buffer.  For each local facet
+// li, rect (local coords [y0,y1) x [x0,x1) of array `which`) goes to host dst at
+// (gy0, gx0) with pitch dpitch.  `pick` selects the device array of a facet.
+struct Piece { int facet; int64_t y0, y1, x0, x1; int64_t gy0, gx0; };
+template <typename Pick>
+static deblur_status gather_pieces(deblur_t h, const std::vector<Piece> &all, Pick pick, float *dst, int64_t dpitch) {
+    // all: pieces of ALL facets (every rank computes the same list)
+    for (const Piece &pc : all) {
+        const int owner = h->plan.facets[pc.facet].owner;
+        const int64_t w = pc.x1 - pc.x0, hh = pc.y1 - pc.y0;
+        if (w <= 0 || hh <= 0) continue;
+        if (owner == h->rank) {
+            const FacetDev &F = h->fh[h->local_index[pc.facet]];
+            int64_t pitch; const float *src = pick(F, pitch);
+            if (h->rank == 0) {
+                if (dst)
+                    CU(cudaMemcpy2DAsync(dst + pc.gy0 * dpitch + pc.gx0, dpitch * 4, src + pc.y0 * pitch + pc.x0,
+                                         pitch * 4, w * 4, hh, cudaMemcpyDeviceToHost, h->stream));
+            } else {
+                float *tmp = nullptr;
+                CU(cudaMallocAsync((void **)&tmp, w * hh * 4, h->stream));
+                CU(cudaMemcpy2DAsync(tmp, w * 4, src + pc.y0 * pitch + pc.x0, pitch * 4, w * 4, hh,
+                                     cudaMemcpyDeviceToDevice, h->stream));
+                NC(ncclSend(tmp, (size_t)(w * hh), ncclFloat, 0, h->comm, h->stream), "gather send", 0);
+                CU(cudaFreeAsync(tmp, h->stream));
+            }
+        } else if (h->rank == 0) {
+            float *tmp = nullptr;
+            CU(cudaMallocAsync((void **)&tmp, w * hh * 4, h->stream));
+            NC(ncclRecv(tmp, (size_t)(w * hh), ncclFloat, owner, h->comm, h->stream), "gather recv", owner);
+            if (dst)
+                CU(cudaMemcpy2DAsync(dst + pc.gy0 * dpitch + pc.gx0, dpitch * 4, tmp, w * 4, w * 4, hh,
+                                     cudaMemcpyDeviceToHost, h->stream));
+            CU(cudaFreeAsync(tmp, h->stream));
+        }
+    }
+    return finish(h);
+}
+
+// owner-computes regions (§8b): observed core [b_k, b_{k+1}); estimate [b_k + c, b_{k+1} + c) with the ends extended
+static void core_range(const Plan &pl, bool rows, int k, bool estimate, int64_t &lo, int64_t &hi) {
+    const int64_t M = rows ? pl.my : pl.mx;
+    const int F = rows ? pl.Fy : pl.Fx;
+    const int64_t c = (pl.P - 1) / 2;
+    lo = (int64_t)k * M / F; hi = (int64_t)(k + 1) * M / F;
+    if (estimate) {
+        lo = (k == 0) ? 0 : lo + c;
+        hi = (k == F - 1) ? (rows ? pl.ny : pl.nx) : hi + c;
+    }
+}
+
+static deblur_status apply_common(deblur_t h, bool adjoint, const float *in, bool in_dev, float *out, bool out_dev) {
+    const Plan &pl = h->plan;
+    if (adjoint && (pl.Fy > 1 || pl.Fx > 1) && pl.O < pl.P - 1)
+        return h->fail(DEBLUR_EINVAL, "apply_HT with several facets needs overlap >= P - 1 (SURVEY §8b)");
+    const cudaMemcpyKind kin = in_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    for (size_t li = 0; li < h->local.size(); ++li) {
+        const FacetPlan &fp = pl.facets[h->local[li]];
+        const FacetDev &F = h->fh[li];
+        if (!adjoint)
+            CU(cudaMemcpy2DAsync(F.g, F.ep * 4, in + fp.ey0 * pl.nx + fp.ex0, pl.nx * 4, F.nx * 4, F.ny, kin, h->stream));
+        else
+            CU(cudaMemcpy2DAsync(F.r, F.op * 4, in + fp.oy0 * pl.mx + fp.ox0, pl.mx * 4, F.mx * 4, F.my, kin, h->stream));
+    }
+    cudaEvent_t ev = nullptr;
+    if (h->conv_path == DEBLUR_CONV_FFT) {
+        if (!adjoint) {
+            h->prof_begin(KC_FFT_H, &ev);
+            CU(fft_H(*h->fft, h->d_facets_alt, 0, FFT_PLAIN, h->stream));
+            h->prof_end(KC_FFT_H, ev);
+        } else {
+            h->prof_begin(KC_FFT_HT, &ev);
+            CU(fft_HT(*h->fft, h->d_facets, h->stream));
+            h->prof_end(KC_FFT_HT, ev);
+        }
+    } else if (!adjoint) {
+        h->prof_begin(KC_H_PLAIN, &ev);
+        CU(launch_H_direct(h->conv_args(h->d_facets_alt, false), H_PLAIN, 0, h->stream));
+        h->prof_end(KC_H_PLAIN, ev);
+    } else {
+        h->prof_begin(KC_HT_PLAIN, &ev);
+        CU(launch_HT_direct(h->conv_args(h->d_facets, true), HT_PLAIN, h->par, 0, h->sc, h->stream));
+        h->prof_end(KC_HT_PLAIN, ev);
+    }
+    std::vector<Piece> pieces;
+    for (const auto &fp : pl.facets) {
+        int64_t y0, y1, x0, x1;
+        core_range(pl, true, fp.fy, adjoint, y0, y1);
+        core_range(pl, false, fp.fx, adjoint, x0, x1);
+        const int64_t oy = adjoint ? fp.ey0 : fp.oy0, ox = adjoint ? fp.ex0 : fp.ox0;
+        pieces.push_back({fp.id, y0 - oy, y1 - oy, x0 - ox, x1 - ox, y0, x0});
+    }
+    const int64_t dp = adjoint ? pl.nx : pl.mx;
+    if (out_dev) {
+        for (const Piece &pc : pieces) {
+            const FacetDev &F = h->fh[h->local_index[pc.facet]];
+            const float *src = adjoint ? F.g : F.r;
+            const int64_t pitch = adjoint ? F.ep : F.op;
+            CU(cudaMemcpy2DAsync(out + pc.gy0 * dp + pc.gx0, dp * 4, src + pc.y0 * pitch + pc.x0, pitch * 4,
+                                 (pc.x1 - pc.x0) * 4, pc.y1 - pc.y0, cudaMemcpyDeviceToDevice, h->stream));
+        }
+        return finish(h);
+    }
+    return gather_pieces(
+        h, pieces,
+        [adjoint](const FacetDev &F, int64_t &pitch) -> const float * {
+            pitch = adjoint ? F.ep : F.op;
+            return adjoint ? F.g : F.r;
+        },
+        out, dp);
+}
+
+extern "C" {
+
+deblur_status deblur_apply_H(deblur_t h, const float *x, float *hx) {
+    deblur_status s = check_state(h);
+    if (s != DEBLUR_OK) return s;
+    if (!x) return h->fail(DEBLUR_EINVAL, "x is NULL");
+    if (h->rank == 0 && !hx) return h->fail(DEBLUR_EINVAL, "hx is NULL on rank 0");
+    return apply_common(h, false, x, false, hx, false);
+}
+
+deblur_status deblur_apply_HT(deblur_t h, const float *r, float *g) {
+    deblur_status s = check_state(h);
+    if (s != DEBLUR_OK) return s;
+    if (!r) return h->fail(DEBLUR_EINVAL, "r is NULL");
+    if (h->rank == 0 && !g) return h->fail(DEBLUR_EINVAL, "g is NULL on rank 0");
+    return apply_common(h, true, r, false, g, false);
+}
+
+deblur_status deblur_apply_H_device(deblur_t h, const float *d_x, float *d_hx) {
+    deblur_status s = check_state(h);
+    if (s != DEBLUR_OK) return s;
+    if (h->world != 1) return h->fail(DEBLUR_ESTATE, "device apply needs world == 1");
+    if (!d_x || !d_hx) return h->fail(DEBLUR_EINVAL, "NULL device pointer");
+    return apply_common(h, false, d_x, true, d_hx, true);
+}
+
+deblur_status deblur_apply_HT_device(deblur_t h, const float *d_r, float *d_g) {
+    deblur_status s = check_state(h);
+    if (s != DEBLUR_OK) return s;
+    if (h->world != 1) return h->fail(DEBLUR_ESTATE, "device apply needs world == 1");
+    if (!d_r || !d_g) return h->fail(DEBLUR_EINVAL, "NULL device pointer");
+    return apply_common(h, true, d_r, true, d_g, true);
+}
+
+deblur_status deblur_state_size(deblur_t h, int64_t *n) {
+    if (!h || !n) return DEBLUR_EINVAL;
+    int64_t t = 0;
+    for (const auto &f : h->plan.facets) t += (f.ey1 - f.ey0) * (f.ex1 - f.ex0);
+    *n = t;
+    return DEBLUR_OK;
+}
+
+static std::vector<int64_t> facet_offsets(const Plan &pl) {
+    std::vector<int64_t> off(pl.facets.size() + 1, 0);
+    for (size_t i = 0; i < pl.facets.size(); ++i)
+        off[i + 1] = off[i] + (pl.facets[i].ey1 - pl.facets[i].ey0) * (pl.facets[i].ex1 - pl.facets[i].ex0);
+    return off;
+}
+
+deblur_status deblur_get_state(deblur_t h, float *xf, float *uf) {
+    deblur_status s = check_state(h);
+    if (s != DEBLUR_OK) return s;
+    const Plan &pl = h->plan;
+    auto off = facet_offsets(pl);
+    for (int which = 0; which < 2; ++which) {
+        float *dst = which == 0 ? xf : uf;
+        if (h->rank == 0 && !dst) return h->fail(DEBLUR_EINVAL, "NULL output on rank 0");
+        // each facet is its own "image" with pitch = its width: use per-facet pieces
+        for (const auto &fp : pl.facets) {
+            const int64_t w = fp.ex1 - fp.ex0, hh = fp.ey1 - fp.ey0;
+            std::vector<Piece> one{{fp.id, 0, hh, 0, w, 0, 0}};
+            const int par = h->par;
+            s = gather_pieces(
+                h, one,
+                [which, par](const FacetDev &F, int64_t &pitch) -> const float * {
+                    pitch = F.ep;
+                    return which == 0 ? F.x[par] : F.u;
+                },
+                dst ? dst + off[fp.id] : nullptr, w);
+            if (s != DEBLUR_OK) return s;
+        }
+    }
+    return DEBLUR_OK;
+}
+
+deblur_status deblur_set_state(deblur_t h, const float *xf, const float *uf) {
+    deblur_status s = check_state(h);
+    if (s != DEBLUR_OK) return s;
+    if (!xf || !uf) return h->fail(DEBLUR_EINVAL, "NULL state array");
+    auto off = facet_offsets(h->plan);
+    for (size_t li = 0; li < h->local.size(); ++li) {
+        const FacetDev &F = h->fh[li];
+        const int64_t o = off[F.id];
+        CU(cudaMemcpy2DAsync(F.x[h->par], F.ep * 4, xf + o, F.nx * 4, F.nx * 4, F.ny, cudaMemcpyHostToDevice, h->stream));
+        CU(cudaMemcpy2DAsync(F.u, F.ep * 4, uf + o, F.nx * 4, F.nx * 4, F.ny, cudaMemcpyHostToDevice, h->stream));
+    }
+    return finish(h);
+}
+
+deblur_status deblur_get_image(deblur_t h, float *x) {
+    deblur_status s = check_state(h);
+    if (s != DEBLUR_OK) return s;
+    const Plan &pl = h->plan;
+    if (h->rank == 0 && !x) return h->fail(DEBLUR_EINVAL, "x is NULL on rank 0");
+    // gather every facet's x to rank 0, then x_hat = sum_f omega^F_f x_f in facet order (A7)
+    int64_t n = 0;
+    deblur_state_size(h, &n);
+    std::vector<float> xs(h->rank == 0 ? (size_t)n : 0);
+    auto off = facet_offsets(pl);
+    for (const auto &fp : pl.facets) {
+        const int64_t w = fp.ex1 - fp.ex0, hh = fp.ey1 - fp.ey0;
+        std::vector<Piece> one{{fp.id, 0, hh, 0, w, 0, 0}};
+        const int par = h->par;
+        s = gather_pieces(
+            h, one,
+            [par](const FacetDev &F, int64_t &pitch) -> const float * {
+                pitch = F.ep;
+                return F.x[par];
+            },
+            h->rank == 0 ? xs.data() + off[fp.id] : nullptr, w);
+        if (s != DEBLUR_OK) return s;
+    }
+    if (h->rank != 0) return DEBLUR_OK;
+    std::fill(x, x + pl.ny * pl.nx, 0.f);
+    for (const auto &fp : pl.facets) {
+        const AxisW ay = {(int)fp.ey0, (int)(fp.ey1 - fp.ey0), (int)(fp.py_e - fp.ey0), (int)(fp.ny_s - fp.ey0),
+                          (int)fp.ey0, (int)fp.py_e, (int)fp.ny_s, (int)fp.ey1};
+        const AxisW ax = {(int)fp.ex0, (int)(fp.ex1 - fp.ex0), (int)(fp.px_e - fp.ex0), (int)(fp.nx_s - fp.ex0),
+                          (int)fp.ex0, (int)fp.px_e, (int)fp.nx_s, (int)fp.ex1};
+        const int64_t w = fp.ex1 - fp.ex0;
+        for (int64_t r = 0; r < fp.ey1 - fp.ey0; ++r) {
+            const float oy = omega_axis(ay, (int)r);
+            for (int64_t q = 0; q < w; ++q)
+                x[(fp.ey0 + r) * pl.nx + fp.ex0 + q] += oy * omega_axis(ax, (int)q) * xs[off[fp.id] + r * w + q];
+        }
+    }
+    return DEBLUR_OK;
+}
+
+deblur_status deblur_reset(deblur_t h, const float *y, const float *x0) {
+    deblur_status s = check_state(h);
+    if (s != DEBLUR_OK) return s;
+    if (!y) return h->fail(DEBLUR_EINVAL, "y is NULL");
+    if ((s = upload_y(h, y)) != DEBLUR_OK) return s;
+    if (!x0) {
+        deblur_params p = h->prm;
+        p.y = y;
+        std::vector<float> x = default_x0(&p);
+        return upload_state_x0(h, x.data());
+    }
+    return upload_state_x0(h, x0);
+}
+
+deblur_status deblur_get_step(deblur_t h, double *tau) {
+    if (!h || !tau) return DEBLUR_EINVAL;
+    *tau = h->tau;
+    return DEBLUR_OK;
+}
+
+deblur_status deblur_get_conv_path(deblur_t h, int32_t *path) {
+    if (!h || !path) return DEBLUR_EINVAL;
+    *path = h->conv_path;
+    return DEBLUR_OK;
+}
+
+deblur_status deblur_set_profiling(deblur_t h, int32_t enable) {
+    if (!h) return DEBLUR_EINVAL;
+    h->prof = enable != 0;
+    return DEBLUR_OK;
+}
+
+deblur_status deblur_kernel_stats(deblur_t h, int32_t *n_classes, int64_t *launches, double *ms) {
+    if (!h || !n_classes) return DEBLUR_EINVAL;
+    const int n = std::min<int>(*n_classes, KC_COUNT);
+    for (int i = 0; i < n; ++i) {
+        if (launches) launches[i] = h->stat_n[i];
+        if (ms) ms[i] = h->stat_ms[i];
+    }
+    *n_classes = KC_COUNT;
+    return DEBLUR_OK;
+}
+
+deblur_status deblur_reset_stats(deblur_t h) {
+    if (!h) return DEBLUR_EINVAL;
+    for (int i = 0; i < KC_COUNT; ++i) { h->stat_n[i] = 0; h->stat_ms[i] = 0; }
+    return DEBLUR_OK;
+}
+
+}  // extern "C"

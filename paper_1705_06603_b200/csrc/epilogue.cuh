@@ -1,0 +1,88 @@
+// epilogue.cuh -- device helpers shared by the direct and FFT paths (internal).
+#pragma once
+#include "device.cuh"
+
+namespace deblur {
+
+constexpr int EPI_NT = 256;
+
+__device__ __forceinline__ double block_sum(double v, double *scratch) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < EPI_NT / 32; ++i) t += scratch[i];
+    return t;
+}
+
+// ----------------------------------------------------------------- shared epilogue
+// TV gradient + prox + projection + dual/band update for one output pixel, reading
+// x from a (TYh+2) x (TXh+2) smem halo tile xh whose element (i, j) holds facet
+// pixel (wrap(y0-1+i), wrap(x0-1+j)).  Returns phi(D x) at the pixel (reg partial).
+__device__ __forceinline__ float update_pixel(const FacetDev &F, const float *xh, int XH, int i, int j, int fy, int fx, float g,
+                              int par, int last, const SolverConst &sc) {
+    const int ny = F.ny, nx = F.nx;
+    const bool neu = sc.tv_boundary == 1;
+    const float e2 = sc.eps * sc.eps;
+    auto X = [&](int a, int b) { return xh[a * XH + b]; };
+    const int fyu = (fy == 0) ? ny - 1 : fy - 1;
+    const int fxl = (fx == 0) ? nx - 1 : fx - 1;
+    // D x at (i,j), (i-1,j), (i,j-1): forward differences, circular or Neumann
+    const float xc = X(i, j);
+    const float dyc = (neu && fy == ny - 1) ? 0.f : X(i + 1, j) - xc;
+    const float dxc = (neu && fx == nx - 1) ? 0.f : X(i, j + 1) - xc;
+    const float dyu = (neu && fyu == ny - 1) ? 0.f : xc - X(i - 1, j);
+    const float dxu = (neu && fx == nx - 1) ? 0.f : X(i - 1, j + 1) - X(i - 1, j);
+    const float dyl = (neu && fy == ny - 1) ? 0.f : X(i + 1, j - 1) - X(i, j - 1);
+    const float dxl = (neu && fxl == nx - 1) ? 0.f : xc - X(i, j - 1);
+    float sc_c, sc_u, sc_l, phi;
+    const float t2c = dyc * dyc + dxc * dxc;
+    if (sc.reg_kind == 0) {
+        const float rc = sqrtf(t2c + e2);
+        sc_c = 1.f / rc;
+        sc_u = 1.f / sqrtf(dyu * dyu + dxu * dxu + e2);
+        sc_l = 1.f / sqrtf(dyl * dyl + dxl * dxl + e2);
+        phi = t2c / (rc + sc.eps);                       // sqrt(t2+e2) - eps without cancellation
+    } else {
+        const float d = sc.eps;
+        const float tc = sqrtf(t2c), tu = sqrtf(dyu * dyu + dxu * dxu), tl = sqrtf(dyl * dyl + dxl * dxl);
+        sc_c = (tc <= d) ? 1.f : d / tc;
+        sc_u = (tu <= d) ? 1.f : d / tu;
+        sc_l = (tl <= d) ? 1.f : d / tl;
+        phi = (tc <= d) ? 0.5f * t2c : d * (tc - 0.5f * d);
+    }
+    // D^T psi(D x): psi_y(p-1) - psi_y(p) + psi_x(q-1) - psi_x(q)
+    const float tdiv = dyu * sc_u - dyc * sc_c + dxl * sc_l - dxc * sc_c;
+    const int64_t o = (int64_t)fy * F.ep + fx;
+    const float uc = F.u[o];
+    const float om = omega_axis(F.ay, fy) * omega_axis(F.ax, fx);
+    const float gt = g + sc.lambda * tdiv + sc.gamma * om * (xc - uc);
+    const float xn = fmaxf(0.f, xc - sc.tau * gt);
+    F.x[par ^ 1][o] = xn;
+    if (last) {
+        const bool shared = fy < F.ay.b_prev || fy >= F.ay.b_next || fx < F.ax.b_prev || fx >= F.ax.b_next;
+        if (!shared)
+            F.u[o] = uc + sc.rho * (xn - uc);      // single owner: zbar = 2x+ - u (Lemma 1 with one term)
+        else
+            F.v[o] = 2.f * xn - uc;                // band value sent to the consensus
+    }
+    return phi;
+}
+
+// stage the (TYh+2) x (TXh+2) circular halo of x[par] for a tile at (y0, x0)
+__device__ __forceinline__ void stage_halo(const FacetDev &F, float *xh, int XH, int YH, int y0, int x0, int par) {
+    const float *__restrict__ x = F.x[par];
+    for (int idx = threadIdx.x; idx < YH * XH; idx += blockDim.x) {
+        const int i = idx / XH, j = idx - i * XH;
+        int fy = y0 - 1 + i, fx = x0 - 1 + j;
+        fy = ((fy % F.ny) + F.ny) % F.ny;
+        fx = ((fx % F.nx) + F.nx) % F.nx;
+        xh[idx] = x[(int64_t)fy * F.ep + fx];
+    }
+}
+
+
+}  // namespace deblur

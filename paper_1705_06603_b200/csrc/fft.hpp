@@ -1,0 +1,31 @@
+// fft.hpp -- hand-written FFT overlap-save path for H / H^T (internal).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+#include "plan.hpp"
+
+namespace deblur {
+
+enum FftMode { FFT_RESIDUAL = 0, FFT_PLAIN = 1, FFT_OBJECTIVE = 2 };
+
+struct FftPlan;
+
+// Measured crossover: true when the FFT path beats the direct stencil for P.
+bool fft_prefer(int P);
+FftPlan *fft_create(const Plan &pl, const std::vector<int> &local, const std::vector<FacetDev> &fh,
+                    const float *d_psfs, const float *d_wy, const float *d_wx, int Gy, int Gx, const float *h_wy,
+                    const float *h_wx, cudaStream_t s, std::string &err);
+void fft_destroy(FftPlan *f);
+// H on every local facet: mode RESIDUAL writes r = w (Hx - y) and data partials,
+// PLAIN writes r = Hx, OBJECTIVE only the partials.
+cudaError_t fft_H(FftPlan &f, const FacetDev *d_facets, int par, int mode, cudaStream_t s);
+// g = H^T r on every local facet (into FacetDev::g).
+cudaError_t fft_HT(FftPlan &f, const FacetDev *d_facets, cudaStream_t s);
+// per-local-facet data partial sums of the last fft_H call (after a stream sync).
+cudaError_t fft_data_partials(FftPlan &f, std::vector<double> &out);
+
+}  // namespace deblur

@@ -1,0 +1,166 @@
+// k_update.cu -- elementwise and band kernels of the hot path.
+//
+//  K4 k_update_from_g (rows a3-a4 when H^T comes from the FFT path): the same
+//      fused TV-gradient / prox / projection / dual epilogue as K2, with g read
+//      from the facet's g array.
+//  K5 k_consensus (row a6, Lemma 1, update PAPER.md:201-202):
+//      on band pixels only, zbar = sum_{f' ascending id} omega^F_{f'} v_{f'} /
+//      sum omega^F_{f'} (A8, A9), u_f += rho (zbar - x+_f).  Neighbour values are
+//      read through View descriptors: the neighbour's v array when it lives on
+//      this GPU, the received halo buffer otherwise.
+//  K6 k_tv_value / k_maxdiff (row a7): fp64 per-block partials of
+//      sum phi(D x) and max |x_f - x_f'| over shared pixels (A22).
+#include "epilogue.cuh"
+#include "kernels.hpp"
+
+namespace deblur {
+namespace {
+
+constexpr int UT_TY = 32, UT_TX = 128;   // update tile (matches the H^T tile grid)
+
+__global__ void __launch_bounds__(EPI_NT) k_update_from_g(const FacetDev *facets, const TileDesc *tiles, int par,
+                                                           int last, SolverConst sc, double *partials) {
+    __shared__ float xh[(UT_TY + 2) * (UT_TX + 2)];
+    __shared__ double red[EPI_NT / 32];
+    const TileDesc t = tiles[blockIdx.x];
+    const FacetDev &F = facets[t.f];
+    constexpr int XH = UT_TX + 2;
+    stage_halo(F, xh, XH, UT_TY + 2, t.y0, t.x0, par);
+    __syncthreads();
+    double rsum = 0.0;
+    for (int idx = threadIdx.x; idx < UT_TY * UT_TX; idx += EPI_NT) {
+        const int ly = idx / UT_TX, lx = idx - ly * UT_TX;
+        const int fy = t.y0 + ly, fx = t.x0 + lx;
+        if (fy >= F.ny || fx >= F.nx) continue;
+        const float g = F.g[(int64_t)fy * F.ep + fx];
+        rsum += (double)update_pixel(F, xh, XH, ly + 1, lx + 1, fy, fx, g, par, last, sc);
+    }
+    if (partials) {
+        const double s = block_sum(rsum, red);
+        if (threadIdx.x == 0) partials[blockIdx.x] = s;
+    }
+}
+
+__global__ void __launch_bounds__(EPI_NT) k_tv_value(const FacetDev *facets, const TileDesc *tiles, int par,
+                                                      SolverConst sc, double *partials) {
+    __shared__ double red[EPI_NT / 32];
+    const TileDesc t = tiles[blockIdx.x];
+    const FacetDev &F = facets[t.f];
+    const float *__restrict__ x = F.x[par];
+    const bool neu = sc.tv_boundary == 1;
+    const float e2 = sc.eps * sc.eps;
+    double rsum = 0.0;
+    for (int idx = threadIdx.x; idx < UT_TY * UT_TX; idx += EPI_NT) {
+        const int fy = t.y0 + idx / UT_TX, fx = t.x0 + idx % UT_TX;
+        if (fy >= F.ny || fx >= F.nx) continue;
+        const int fy1 = (fy + 1 == F.ny) ? 0 : fy + 1, fx1 = (fx + 1 == F.nx) ? 0 : fx + 1;
+        const float xc = x[(int64_t)fy * F.ep + fx];
+        const float dy = (neu && fy == F.ny - 1) ? 0.f : x[(int64_t)fy1 * F.ep + fx] - xc;
+        const float dx = (neu && fx == F.nx - 1) ? 0.f : x[(int64_t)fy * F.ep + fx1] - xc;
+        const float t2 = dy * dy + dx * dx;
+        float phi;
+        if (sc.reg_kind == 0) {
+            phi = t2 / (sqrtf(t2 + e2) + sc.eps);
+        } else {
+            const float tt = sqrtf(t2);
+            phi = (tt <= sc.eps) ? 0.5f * t2 : sc.eps * (tt - 0.5f * sc.eps);
+        }
+        rsum += (double)phi;
+    }
+    const double s = block_sum(rsum, red);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+__device__ __forceinline__ float view_at(const View &v, int par, int gy, int gx) {
+    return v.base[par][(int64_t)(gy - v.y0) * v.pitch + (gx - v.x0)];
+}
+
+// grid: x = chunks of 256 pixels, y = rect index
+__global__ void __launch_bounds__(256) k_consensus(const FacetDev *facets, const BandRect *rects, int par, float rho) {
+    const BandRect R = rects[blockIdx.y];
+    const FacetDev &F = facets[R.f];
+    const int w = R.x1 - R.x0;
+    const int64_t n = (int64_t)(R.y1 - R.y0) * w;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+        const int ly = R.y0 + (int)(idx / w), lx = R.x0 + (int)(idx % w);
+        const int gy = F.ey0 + ly, gx = F.ex0 + lx;
+        const int dy0 = (ly < F.ay.b_prev) ? -1 : 0, dy1 = (ly >= F.ay.b_next) ? 1 : 0;
+        const int dx0 = (lx < F.ax.b_prev) ? -1 : 0, dx1 = (lx >= F.ax.b_next) ? 1 : 0;
+        float num = 0.f, den = 0.f;
+        // ascending facet id = lexicographic (dy, dx) (A9)
+        for (int dy = dy0; dy <= dy1; ++dy)
+            for (int dx = dx0; dx <= dx1; ++dx) {
+                const Neighbour &nb = F.nb[dy + 1][dx + 1];
+                const float om = omega_axis(nb.ay, gy - nb.ay.e0) * omega_axis(nb.ax, gx - nb.ax.e0);
+                num += om * view_at(nb.v, par, gy, gx);
+                den += om;
+            }
+        const float zbar = num / den;
+        const int64_t o = (int64_t)ly * F.ep + lx;
+        F.u[o] += rho * (zbar - F.x[par][o]);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_maxdiff(const FacetDev *facets, const BandRect *rects, int par,
+                                                 double *partials) {
+    __shared__ float red[8];
+    const BandRect R = rects[blockIdx.x];
+    const FacetDev &F = facets[R.f];
+    const int w = R.x1 - R.x0;
+    const int64_t n = (int64_t)(R.y1 - R.y0) * w;
+    float m = 0.f;
+    for (int64_t idx = threadIdx.x; idx < n; idx += blockDim.x) {
+        const int ly = R.y0 + (int)(idx / w), lx = R.x0 + (int)(idx % w);
+        const int gy = F.ey0 + ly, gx = F.ex0 + lx;
+        const int dy0 = (ly < F.ay.b_prev) ? -1 : 0, dy1 = (ly >= F.ay.b_next) ? 1 : 0;
+        const int dx0 = (lx < F.ax.b_prev) ? -1 : 0, dx1 = (lx >= F.ax.b_next) ? 1 : 0;
+        const float xs = F.x[par][(int64_t)ly * F.ep + lx];
+        for (int dy = dy0; dy <= dy1; ++dy)
+            for (int dx = dx0; dx <= dx1; ++dx) {
+                if (dy == 0 && dx == 0) continue;
+                m = fmaxf(m, fabsf(xs - view_at(F.nb[dy + 1][dx + 1].x, par, gy, gx)));
+            }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_down_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int i = 0; i < 8; ++i) t = fmaxf(t, red[i]);
+        partials[blockIdx.x] = (double)t;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_update_from_g(const FacetDev *facets, const TileDesc *tiles, int ntiles, int, int par, int last,
+                                 const SolverConst &sc, double *partials, cudaStream_t s) {
+    if (!ntiles) return cudaSuccess;
+    k_update_from_g<<<ntiles, EPI_NT, 0, s>>>(facets, tiles, par, last, sc, partials);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tv_value(const FacetDev *facets, const TileDesc *tiles, int ntiles, int, int par,
+                            const SolverConst &sc, double *partials, cudaStream_t s) {
+    if (!ntiles) return cudaSuccess;
+    k_tv_value<<<ntiles, EPI_NT, 0, s>>>(facets, tiles, par, sc, partials);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_consensus(const FacetDev *facets, const BandRect *rects, int nrect, int par, float rho,
+                             cudaStream_t s) {
+    if (!nrect) return cudaSuccess;
+    dim3 grid(64, nrect);
+    k_consensus<<<grid, 256, 0, s>>>(facets, rects, par, rho);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_maxdiff(const FacetDev *facets, const BandRect *rects, int nrect, int par, double *partials,
+                           cudaStream_t s) {
+    if (!nrect) return cudaSuccess;
+    k_maxdiff<<<nrect, 256, 0, s>>>(facets, rects, par, partials);
+    return cudaGetLastError();
+}
+
+}  // namespace deblur

@@ -1,0 +1,214 @@
+"""GPU parity: libdeblur (through the C ABI) vs the fp64 oracle on the same
+seeded inputs.  Bars (BASELINE.json north_star): rel-L2 <= 1e-5 for H / H^T,
+<= 1e-4 for the objective, <= 1e-3 for the iterate after the fixed iteration
+count.  rel-L2(a, b) = |a - b|_2 / |b|_2 with b the oracle."""
+import numpy as np
+import pytest
+import scipy.signal
+
+import synth
+from oracle import Operator, from_problem
+from paper_1705_06603_b200 import deblur as D
+
+pytestmark = pytest.mark.gpu
+
+H_TOL = 1e-5
+OBJ_TOL = 1e-4
+IT_TOL = 1e-3
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def oracle_op(pb):
+    return Operator(pb.psfs, pb.wy, pb.wx)
+
+
+def rand_x(pb, seed=0):
+    rng = np.random.default_rng(seed)
+    # star-field-like non-negative test image: background + sparse bright pixels
+    x = 0.05 + 0.02 * rng.random((pb.ny, pb.nx))
+    m = rng.random((pb.ny, pb.nx)) < 0.01
+    x[m] += rng.uniform(0.2, 1.0, m.sum())
+    return x.astype(np.float32)
+
+
+def rand_r(pb, seed=1):
+    return np.random.default_rng(seed).standard_normal((pb.my, pb.mx)).astype(np.float32)
+
+
+# ------------------------------------------------------------------ H / H^T
+OP_CASES = [
+    # (config k, n, facets, overlap, path)
+    (1, None, (1, 1), 0),
+    (1, None, (2, 2), 16),
+    (2, None, (2, 2), 64),
+    (2, 300, (3, 2), 40),          # ragged tiles, 6 facets
+    (3, 1024, (2, 2), 128),        # P = 63: blocked accumulation matters (A24)
+]
+
+
+@pytest.mark.parametrize("k,n,facets,O", OP_CASES)
+def test_apply_H_HT_parity(k, n, facets, O):
+    pb = synth.make_config(k, n=n, facets=facets, overlap=O)
+    op = oracle_op(pb)
+    x, r = rand_x(pb), rand_r(pb)
+    with D.Deblur.from_problem(pb, conv_path=D.CONV_DIRECT) as dev:
+        hx = dev.apply_H(x)
+        g = dev.apply_HT(r)
+    assert rel_l2(hx, op.H(x)) <= H_TOL
+    assert rel_l2(g, op.HT(r)) <= H_TOL
+
+
+@pytest.mark.parametrize("P,G,shape", [(1, 2, (37, 45)), (3, 1, (20, 300)), (7, 3, (131, 259)),
+                                       (15, 2, (256, 129)), (127, 4, (400, 300))])
+def test_apply_parity_odd_shapes(P, G, shape):
+    """Ragged tails, P = 1 (identity-like), a tile-width-thin image, P = 127."""
+    ny, nx = shape
+    rng = np.random.default_rng(P)
+    psfs = rng.uniform(0, 1, (G * G, P, P)).astype(np.float32)
+    psfs /= psfs.sum(axis=(1, 2), keepdims=True)
+    wy, wx = synth.hat_weights(ny, G).astype(np.float32), synth.hat_weights(nx, G).astype(np.float32)
+    my, mx = ny - P + 1, nx - P + 1
+    y = rng.uniform(0, 1, (my, mx)).astype(np.float32)
+    params, keep = D.make_params(psfs, wy, wx, y, conv_path=D.CONV_DIRECT)
+    x = rng.uniform(0, 1, (ny, nx)).astype(np.float32)
+    r = rng.standard_normal((my, mx)).astype(np.float32)
+    op = Operator(psfs, wy, wx)
+    with D.Deblur(params, keep) as dev:
+        assert rel_l2(dev.apply_H(x), op.H(x)) <= H_TOL
+        assert rel_l2(dev.apply_HT(r), op.HT(r)) <= H_TOL
+
+
+def test_gpu_adjoint_identity():
+    pb = synth.make_config(2, n=512, facets=(1, 1), overlap=0)
+    x, r = rand_x(pb, 3), rand_r(pb, 4)
+    with D.Deblur.from_problem(pb, conv_path=D.CONV_DIRECT) as dev:
+        lhs = float(np.dot(dev.apply_H(x).ravel().astype(np.float64), r.ravel()))
+        rhs = float(np.dot(x.ravel().astype(np.float64), dev.apply_HT(r).ravel()))
+    assert abs(lhs - rhs) <= 1e-5 * np.linalg.norm(x) * np.linalg.norm(r)
+
+
+def test_gpu_identical_and_delta_psfs():
+    rng = np.random.default_rng(7)
+    n, P, G = 200, 15, 3
+    h = rng.uniform(0, 1, (P, P))
+    h /= h.sum()
+    wy = synth.hat_weights(n, G).astype(np.float32)
+    x = rng.uniform(0, 1, (n, n)).astype(np.float32)
+    y = np.zeros((n - P + 1, n - P + 1), np.float32)
+    params, keep = D.make_params(np.repeat(h[None], G * G, 0), wy, wy, y, conv_path=D.CONV_DIRECT)
+    with D.Deblur(params, keep) as dev:
+        ref = scipy.signal.convolve2d(x.astype(np.float64), h.astype(np.float32).astype(np.float64), mode="valid")
+        assert rel_l2(dev.apply_H(x), ref) <= H_TOL
+    delta = np.zeros((G * G, P, P), np.float32)
+    delta[:, P // 2, P // 2] = 1
+    params, keep = D.make_params(delta, wy, wy, y, conv_path=D.CONV_DIRECT)
+    with D.Deblur(params, keep) as dev:
+        c = P // 2
+        assert rel_l2(dev.apply_H(x), x[c:n - c, c:n - c]) <= 1e-6
+
+
+@pytest.mark.parametrize("k,count", [(3, 4000), (4, 3000)])
+def test_apply_full_size_sampled(k, count):
+    """BASELINE full sizes (c3 4096^2, c4 16384^2), bench launch configuration,
+    checked on sampled pixels the oracle evaluates one by one."""
+    pb = synth.make_config(k)
+    rng = np.random.default_rng(k)
+    x = (0.05 + rng.random((pb.ny, pb.nx), dtype=np.float32) * 0.5).astype(np.float32)
+    r = rng.standard_normal((pb.my, pb.mx), dtype=np.float32)
+    op = oracle_op(pb)
+    with D.Deblur.from_problem(pb, conv_path=D.CONV_DIRECT) as dev:
+        hx = dev.apply_H(x)
+        g = dev.apply_HT(r)
+    oi, oj = rng.integers(0, pb.my, count), rng.integers(0, pb.mx, count)
+    # include facet seams and image borders
+    oi[:8] = [0, pb.my - 1, 0, pb.my - 1, pb.my // 2, pb.my // 4, 1, pb.my - 2]
+    ref = op.H_points(x, oi, oj)
+    assert rel_l2(hx[oi, oj], ref) <= H_TOL
+    ei, ej = rng.integers(0, pb.ny, count), rng.integers(0, pb.nx, count)
+    ei[:4] = [0, pb.ny - 1, 31, pb.ny - 32]
+    ref = op.HT_points(r, ei, ej)
+    assert rel_l2(g[ei, ej], ref) <= H_TOL
+
+
+# ------------------------------------------------------------------ iterate
+def run_pair(pb, iters, **over):
+    orc = from_problem(pb, **{k: v for k, v in over.items() if k in ("inner_steps", "reg_kind", "tv_boundary")})
+    kw = dict(conv_path=D.CONV_DIRECT, tau=orc.tau)
+    kw.update({k: v for k, v in over.items() if k in ("inner_steps", "reg_kind", "tv_boundary")})
+    with D.Deblur.from_problem(pb, **kw) as dev:
+        obj0 = dev.objective()
+        dev.iterate(iters)
+        xs, us = dev.get_state()
+        obj = dev.objective()
+        img = dev.get_image()
+    ref0 = orc.objective()
+    orc.iterate(iters)
+    xr, ur = orc.state()
+    return dict(x=(xs, xr), u=(us, ur), obj=(obj, orc.objective()), obj0=(obj0, ref0), img=(img, orc.image()))
+
+
+def check_pair(res):
+    assert rel_l2(*res["x"]) <= IT_TOL, rel_l2(*res["x"])
+    assert rel_l2(*res["u"]) <= IT_TOL, rel_l2(*res["u"])
+    assert rel_l2(*res["img"]) <= IT_TOL
+    for (a, b) in (res["obj0"], res["obj"]):
+        for i in range(3):
+            assert abs(a[i] - b[i]) <= OBJ_TOL * abs(b[i]) + 1e-12, (i, a[i], b[i])
+        assert abs(a[3] - b[3]) <= IT_TOL * max(1.0, np.abs(res["x"][1]).max())
+    assert res["x"][0].min() >= 0.0
+
+
+def test_iterate_c1_full():
+    pb = synth.make_config(1)
+    check_pair(run_pair(pb, pb.iters))
+
+
+def test_iterate_c2_full():
+    pb = synth.make_config(2)
+    check_pair(run_pair(pb, pb.iters))
+
+
+@pytest.mark.parametrize("over", [dict(inner_steps=2), dict(reg_kind=1), dict(tv_boundary=1)])
+def test_iterate_variants_ragged(over):
+    pb = synth.make_config(2, n=300, facets=(3, 2), overlap=40)
+    check_pair(run_pair(pb, 15, **over))
+
+
+def test_iterate_c3_small_mixed_noise():
+    """per-pixel W (A21), P = 63, 2x4 facets."""
+    pb = synth.make_config(3, n=1024, overlap=64)
+    check_pair(run_pair(pb, 10))
+
+
+def test_default_tau_matches_oracle():
+    pb = synth.make_config(3, n=512, overlap=64, facets=(2, 2))
+    with D.Deblur.from_problem(pb, conv_path=D.CONV_DIRECT) as dev:
+        t = dev.tau
+    assert t == pytest.approx(from_problem(pb).tau, rel=1e-12)
+
+
+def test_determinism_and_state_roundtrip():
+    pb = synth.make_config(2, n=400, facets=(2, 2), overlap=40)
+    with D.Deblur.from_problem(pb, conv_path=D.CONV_DIRECT) as dev:
+        x0, u0 = dev.get_state()
+        dev.iterate(5)
+        xa, ua = dev.get_state()
+        dev.set_state(x0, u0)
+        dev.iterate(5)
+        xb, ub = dev.get_state()
+    assert np.array_equal(xa, xb) and np.array_equal(ua, ub)
+
+
+def test_zero_data_stays_zero():
+    pb = synth.make_config(1, n=128, facets=(2, 2), overlap=16)
+    pb.y[:] = 0
+    pb.x0 = np.zeros((pb.ny, pb.nx), np.float32)
+    with D.Deblur.from_problem(pb, conv_path=D.CONV_DIRECT) as dev:
+        dev.iterate(3)
+        x, u = dev.get_state()
+    assert np.abs(x).max() == 0 and np.abs(u).max() == 0
