@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""Benchmark: one full distributed iteration of facet-consensus deblurring
+(BASELINE.json metric "Mpixel-iterations/s"), on BASELINE.json configs[3]
+("c4": 16384^2, 16x16 grid of 63x63 Moffat PSFs, 4x2 facets, 128-px overlap)
+unless --config says otherwise.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+
+A step = deblur_iterate(1): per facet one Local-Solver step (H + residual,
+H^T + TV + prox + projection) then halo exchange + consensus.  Inputs are
+resident in HBM before the timed region; the state (~9 GB at c4) is far larger
+than L2, so no flush is needed between steps.  Time = CUDA events on the
+library's own stream, barrier + synchronize on both sides, max over ranks.
+`--impl reference` times the fp64 CPU oracle (the only reference this tier has)
+on a bounded crop of the same workload.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+NOMINAL_SMS = 148
+FMA_PER_SM_CLK = 128
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    try:
+        return json.load(open(MEASURED))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").strip().splitlines():
+            f = [s.strip() for s in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def algorithmic_fma(pb, boxes, which: str) -> float:
+    """a*P^2 FMA per output pixel, a = #{k : omega_k(pixel) != 0}.
+    H: output = observed pixel, omega at its centre (i+c, j+c); H^T: estimate pixel."""
+    c = (pb.P - 1) // 2
+    nzy = (pb.wy != 0).sum(axis=0).astype(np.float64)    # active grid rows per estimate row
+    nzx = (pb.wx != 0).sum(axis=0).astype(np.float64)
+    cy, cx = np.concatenate([[0], np.cumsum(nzy)]), np.concatenate([[0], np.cumsum(nzx)])
+    tot = 0.0
+    for b in boxes:
+        oy0, oy1, ox0, ox1, ey0, ey1, ex0, ex1 = [int(v) for v in b]
+        if which == "H":
+            ry = cy[oy1 + c] - cy[oy0 + c]
+            rx = cx[ox1 + c] - cx[ox0 + c]
+        else:
+            ry = cy[ey1] - cy[ey0]
+            rx = cx[ex1] - cx[ex0]
+        tot += ry * rx
+    return tot * pb.P * pb.P
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    from paper_1705_06603_b200 import deblur as D
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    pb = synth.make_config(args.config)
+    nid = None
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            t = torch.frombuffer(bytearray(D.nccl_id()), dtype=torch.uint8).clone()
+        dist.broadcast(t, 0)
+        nid = bytes(t.tolist())
+    path = {"direct": D.CONV_DIRECT, "fft": D.CONV_FFT, "auto": D.CONV_AUTO}[args.path]
+    params, keep = D.problem_params(pb, conv_path=path, rank=rank, world=world, device=local, nccl_id_bytes=nid)
+    dev = D.Deblur(params, keep)
+    boxes, owner = D.plan_facets(params)
+    stream = torch.cuda.ExternalStream(dev.stream)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    dev.iterate(args.warmup)
+    dev.set_profiling(True)
+    dev.reset_stats()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        dev.iterate(args.steps)
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    stats = dev.kernel_stats()
+    dev.set_profiling(False)
+    t = torch.tensor([ms], dtype=torch.float64)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    npix = pb.ny * pb.nx
+    value = npix * args.steps / (ms / 1e3) / 1e6
+
+    # dominant kernel roofline (this rank's launches; per-launch averages)
+    kern = {k: v for k, v in stats.items() if v[0] > 0 and k != "halo_exchange"}
+    launches = sum(v[0] for v in kern.values())
+    dom = max(kern, key=lambda k: kern[k][1])
+    n_dom, ms_dom = kern[dom]
+    pk = peaks()
+    my_boxes = [b for b, o in zip(boxes, owner) if o == rank]
+    roofline = None
+    if dom in ("H_direct_residual", "HT_direct_update"):
+        fma = algorithmic_fma(pb, my_boxes, "H" if dom.startswith("H_") else "HT")
+        achieved = 2 * fma / (ms_dom / n_dom / 1e3) / 1e12
+        peak = NOMINAL_SMS * FMA_PER_SM_CLK * 2 * pk.get("sm_max_mhz", 1965.0) / 1e6
+        roofline = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
+                    "frac": round(achieved / peak, 4), "traffic": None,
+                    "kernel": dom, "ms_per_launch": round(ms_dom / n_dom, 4),
+                    "peak_source": "148 SM x 128 FP32 FMA/clk x 2 x sm_max_mhz (guide unit counts)"}
+    else:
+        # HBM-bound kernels: algorithmic bytes per launch
+        roofline = {"bound": "hbm", "achieved": None, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": None,
+                    "traffic": None, "kernel": dom, "ms_per_launch": round(ms_dom / n_dom, 4)}
+    breakdown = {k: {"launches": v[0], "ms_per_launch": round(v[1] / max(v[0], 1), 4),
+                     "share": round(v[1] / max(sum(x[1] for x in kern.values()), 1e-9), 4)} for k, v in kern.items()}
+
+    # end to end through the C ABI with host buffers: reset(y from pinned host) + K iterations + image D2H
+    y_pin = torch.from_numpy(pb.y).pin_memory()
+    img_pin = torch.empty((pb.ny, pb.nx), dtype=torch.float32).pin_memory() if rank == 0 else None
+    barrier()
+    t0 = time.perf_counter()
+    dev.reset(y_pin.numpy())                      # pinned host buffer, no staging copy
+    dev.iterate(args.steps)
+    dev.get_image(out=img_pin.numpy() if img_pin is not None else None)
+    barrier()
+    te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = {"value": round(npix * args.steps / float(te.item()) / 1e6, 3), "unit": "Mpixel-iterations/s",
+           "h2d_bytes_per_step": int(pb.y.nbytes // args.steps),
+           "d2h_bytes_per_step": int(npix * 4 // args.steps),
+           "job": f"deblur_reset(y host pinned) + deblur_iterate({args.steps}) + deblur_get_image(host pinned)",
+           "seconds": round(float(te.item()), 3)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(pb, args.cpu_seconds)
+
+    if rank == 0:
+        clocks = clk.summary()
+        cfg = dict(synth.CONFIGS[args.config])
+        line = {
+            "metric": "Mpixel-iterations/s (full distributed iteration)",
+            "value": round(value, 3), "unit": "Mpixel-iterations/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded star field, synth/)",
+            "config": {"workload": f"c{args.config}", "image": f"{pb.ny}x{pb.nx}", "psf": f"{pb.P}x{pb.P}",
+                       "psf_grid": f"{pb.gy}x{pb.gx}", "facets": f"{pb.fy}x{pb.fx}", "overlap": pb.overlap,
+                       "lambda": pb.lam, "eps": pb.eps, "iterations_per_step": 1, "inner_steps": pb.inner_steps,
+                       "conv_path": {1: "direct", 2: "fft"}[dev.conv_path],
+                       "l2": "no flush: resident state >> 126 MB L2", "parallelism": f"facets over {world} GPU(s)"},
+            "gpu_launches": int(launches),
+            "roofline": roofline,
+            "kernels": breakdown,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    dev.close()
+
+
+def oracle_sample(pb, n: int):
+    """A bounded crop of the workload for the oracle: the n x n block of the
+    estimate domain starting at (N/4, N/4) (so it straddles PSF-grid cells like
+    the bulk of the image) with its PSFs, weights and observed pixels, one facet."""
+    from oracle import solver
+    P = pb.P
+    m = n - P + 1
+    o = min(pb.ny // 4, pb.ny - n)
+    prm = solver.Params(lam=pb.lam, eps=pb.eps, gamma=pb.gamma, rho=pb.rho, reg_kind=pb.reg_kind,
+                        tv_boundary=pb.tv_boundary, inner_steps=pb.inner_steps)
+    w = pb.noise_w[o:o + m, o:o + m] if pb.noise_w is not None else np.float64(np.float32(pb.noise_w_scalar))
+    return solver.Deblur(pb.psfs, pb.wy[:, o:o + n], pb.wx[:, o:o + n], pb.y[o:o + m, o:o + m], w, 1, 1, 0, prm)
+
+
+def cpu_baseline(pb, seconds: float):
+    n = min(pb.ny, 512)
+    d = oracle_sample(pb, n)
+    t0 = time.perf_counter()
+    d.iterate(1)
+    dt = time.perf_counter() - t0
+    # scale the crop so one iteration takes ~seconds/2, then time 2 iterations
+    n2 = int(min(pb.ny, max(n, n * math.sqrt(max(seconds / 2 / dt, 1.0)))))
+    n2 = max(pb.P + 1, n2 - n2 % 2)
+    d = oracle_sample(pb, n2)
+    t0 = time.perf_counter()
+    d.iterate(2)
+    dt = time.perf_counter() - t0
+    return {"value": round(n2 * n2 * 2 / dt / 1e6, 4), "unit": "Mpixel-iterations/s",
+            "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)), "kind": "oracle",
+            "sample": f"fp64 oracle, 2 iterations on the {n2}x{n2} crop at (N/4, N/4) of c{args_config(pb)} (1 facet)",
+            "seconds": round(dt, 2)}
+
+
+def args_config(pb):
+    return pb.name.lstrip("c").split("@")[0]
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    pb = synth.make_config(args.config)
+    n = min(pb.ny, args.ref_crop)
+    d = oracle_sample(pb, n)
+    d.iterate(args.warmup)
+    t0 = time.perf_counter()
+    d.iterate(args.steps)
+    dt = time.perf_counter() - t0
+    value = n * n * args.steps / dt / 1e6
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    sample = f"fp64 oracle, {n}x{n} crop at (N/4, N/4) of c{args.config} (1 facet), {args.steps} iterations"
+    line = {"impl": "reference", "metric": "Mpixel-iterations/s (full distributed iteration)",
+            "value": round(value, 4), "unit": "Mpixel-iterations/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded star field, synth/)",
+            "config": {"workload": f"c{args.config}", "sample": sample},
+            "cpu_baseline": {"value": round(value, 4), "unit": "Mpixel-iterations/s", "cores": cores,
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": round(value, 4), "unit": "Mpixel-iterations/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--path", choices=["auto", "direct", "fft"], default="auto")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-crop", type=int, default=1024)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -177,6 +177,10 @@ DEBLUR_API deblur_status deblur_kernel_stats(deblur_t h, int32_t *n_classes, int
 DEBLUR_API const char *deblur_kernel_name(int32_t cls);
 DEBLUR_API deblur_status deblur_reset_stats(deblur_t h);
 
+/* The cudaStream_t (as void*) every kernel of this handle is launched on, so a
+ * caller can bracket calls with CUDA events on the launching stream. */
+DEBLUR_API deblur_status deblur_get_stream(deblur_t h, void **stream);
+
 /* Conv path actually used (deblur_conv_path, never AUTO). */
 DEBLUR_API deblur_status deblur_get_conv_path(deblur_t h, int32_t *path);
 

@@ -1017,6 +1017,12 @@ deblur_status deblur_get_step(deblur_t h, double *tau) {
     return DEBLUR_OK;
 }
 
+deblur_status deblur_get_stream(deblur_t h, void **stream) {
+    if (!h || !stream) return DEBLUR_EINVAL;
+    *stream = (void *)h->stream;
+    return DEBLUR_OK;
+}
+
 deblur_status deblur_get_conv_path(deblur_t h, int32_t *path) {
     if (!h || !path) return DEBLUR_EINVAL;
     *path = h->conv_path;

@@ -84,6 +84,7 @@ def lib():
             "deblur_kernel_name": ([ctypes.c_int32], ctypes.c_char_p),
             "deblur_reset_stats": ([h], ctypes.c_int),
             "deblur_get_conv_path": ([h, _ip], ctypes.c_int),
+            "deblur_get_stream": ([h, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
             "deblur_plan_facets": ([ctypes.POINTER(Params), _ip, _lp, _ip], ctypes.c_int),
             "deblur_plan_messages": ([ctypes.POINTER(Params), ctypes.c_int32, _ip, _lp], ctypes.c_int),
             "deblur_last_error": ([h], ctypes.c_char_p),
@@ -100,7 +101,7 @@ EXPORTED = ["deblur_nccl_id", "deblur_create", "deblur_destroy", "deblur_apply_H
             "deblur_apply_H_device", "deblur_apply_HT_device", "deblur_iterate", "deblur_objective",
             "deblur_get_image", "deblur_state_size", "deblur_get_state", "deblur_set_state", "deblur_reset",
             "deblur_get_step", "deblur_set_profiling", "deblur_kernel_stats", "deblur_kernel_name",
-            "deblur_reset_stats", "deblur_get_conv_path", "deblur_plan_facets", "deblur_plan_messages",
+            "deblur_reset_stats", "deblur_get_conv_path", "deblur_get_stream", "deblur_plan_facets", "deblur_plan_messages",
             "deblur_last_error"]
 
 
@@ -252,8 +253,11 @@ class Deblur:
         self._c(self._lib.deblur_objective(self._h, out))
         return tuple(out)
 
-    def get_image(self) -> Optional[np.ndarray]:
-        out = np.empty((self.ny, self.nx), np.float32) if self.rank == 0 else None
+    def get_image(self, out: Optional[np.ndarray] = None) -> Optional[np.ndarray]:
+        if out is None and self.rank == 0:
+            out = np.empty((self.ny, self.nx), np.float32)
+        if out is not None:
+            assert out.dtype == np.float32 and out.shape == (self.ny, self.nx) and out.flags.c_contiguous
         self._c(self._lib.deblur_get_image(self._h, _ptr(out)))
         return out
 
@@ -289,6 +293,12 @@ class Deblur:
         p = ctypes.c_int32(0)
         self._c(self._lib.deblur_get_conv_path(self._h, ctypes.byref(p)))
         return p.value
+
+    @property
+    def stream(self) -> int:
+        s = ctypes.c_void_p()
+        self._c(self._lib.deblur_get_stream(self._h, ctypes.byref(s)))
+        return s.value or 0
 
     # --- instrumentation -----------------------------------------------------
     def set_profiling(self, on: bool):
