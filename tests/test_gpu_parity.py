@@ -51,21 +51,27 @@ OP_CASES = [
 ]
 
 
+PATHS = [D.CONV_DIRECT, D.CONV_FFT]
+
+
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("k,n,facets,O", OP_CASES)
-def test_apply_H_HT_parity(k, n, facets, O):
+def test_apply_H_HT_parity(k, n, facets, O, path):
     pb = synth.make_config(k, n=n, facets=facets, overlap=O)
     op = oracle_op(pb)
     x, r = rand_x(pb), rand_r(pb)
-    with D.Deblur.from_problem(pb, conv_path=D.CONV_DIRECT) as dev:
+    with D.Deblur.from_problem(pb, conv_path=path) as dev:
+        assert dev.conv_path == path
         hx = dev.apply_H(x)
         g = dev.apply_HT(r)
     assert rel_l2(hx, op.H(x)) <= H_TOL
     assert rel_l2(g, op.HT(r)) <= H_TOL
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("P,G,shape", [(1, 2, (37, 45)), (3, 1, (20, 300)), (7, 3, (131, 259)),
-                                       (15, 2, (256, 129)), (127, 4, (400, 300))])
-def test_apply_parity_odd_shapes(P, G, shape):
+                                       (15, 2, (256, 129)), (127, 4, (400, 300)), (63, 3, (700, 1100))])
+def test_apply_parity_odd_shapes(P, G, shape, path):
     """Ragged tails, P = 1 (identity-like), a tile-width-thin image, P = 127."""
     ny, nx = shape
     rng = np.random.default_rng(P)
@@ -74,7 +80,7 @@ def test_apply_parity_odd_shapes(P, G, shape):
     wy, wx = synth.hat_weights(ny, G).astype(np.float32), synth.hat_weights(nx, G).astype(np.float32)
     my, mx = ny - P + 1, nx - P + 1
     y = rng.uniform(0, 1, (my, mx)).astype(np.float32)
-    params, keep = D.make_params(psfs, wy, wx, y, conv_path=D.CONV_DIRECT)
+    params, keep = D.make_params(psfs, wy, wx, y, conv_path=path)
     x = rng.uniform(0, 1, (ny, nx)).astype(np.float32)
     r = rng.standard_normal((my, mx)).astype(np.float32)
     op = Operator(psfs, wy, wx)
@@ -112,8 +118,9 @@ def test_gpu_identical_and_delta_psfs():
         assert rel_l2(dev.apply_H(x), x[c:n - c, c:n - c]) <= 1e-6
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("k,count", [(3, 4000), (4, 3000)])
-def test_apply_full_size_sampled(k, count):
+def test_apply_full_size_sampled(k, count, path):
     """BASELINE full sizes (c3 4096^2, c4 16384^2), bench launch configuration,
     checked on sampled pixels the oracle evaluates one by one."""
     pb = synth.make_config(k)
@@ -121,7 +128,7 @@ def test_apply_full_size_sampled(k, count):
     x = (0.05 + rng.random((pb.ny, pb.nx), dtype=np.float32) * 0.5).astype(np.float32)
     r = rng.standard_normal((pb.my, pb.mx), dtype=np.float32)
     op = oracle_op(pb)
-    with D.Deblur.from_problem(pb, conv_path=D.CONV_DIRECT) as dev:
+    with D.Deblur.from_problem(pb, conv_path=path) as dev:
         hx = dev.apply_H(x)
         g = dev.apply_HT(r)
     oi, oj = rng.integers(0, pb.my, count), rng.integers(0, pb.mx, count)
@@ -136,9 +143,9 @@ def test_apply_full_size_sampled(k, count):
 
 
 # ------------------------------------------------------------------ iterate
-def run_pair(pb, iters, **over):
+def run_pair(pb, iters, path=D.CONV_DIRECT, **over):
     orc = from_problem(pb, **{k: v for k, v in over.items() if k in ("inner_steps", "reg_kind", "tv_boundary")})
-    kw = dict(conv_path=D.CONV_DIRECT, tau=orc.tau)
+    kw = dict(conv_path=path, tau=orc.tau)
     kw.update({k: v for k, v in over.items() if k in ("inner_steps", "reg_kind", "tv_boundary")})
     with D.Deblur.from_problem(pb, **kw) as dev:
         obj0 = dev.objective()
@@ -163,26 +170,30 @@ def check_pair(res):
     assert res["x"][0].min() >= 0.0
 
 
-def test_iterate_c1_full():
+@pytest.mark.parametrize("path", PATHS)
+def test_iterate_c1_full(path):
     pb = synth.make_config(1)
-    check_pair(run_pair(pb, pb.iters))
+    check_pair(run_pair(pb, pb.iters, path))
 
 
-def test_iterate_c2_full():
+@pytest.mark.parametrize("path", PATHS)
+def test_iterate_c2_full(path):
     pb = synth.make_config(2)
-    check_pair(run_pair(pb, pb.iters))
+    check_pair(run_pair(pb, pb.iters, path))
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("over", [dict(inner_steps=2), dict(reg_kind=1), dict(tv_boundary=1)])
-def test_iterate_variants_ragged(over):
+def test_iterate_variants_ragged(over, path):
     pb = synth.make_config(2, n=300, facets=(3, 2), overlap=40)
-    check_pair(run_pair(pb, 15, **over))
+    check_pair(run_pair(pb, 15, path, **over))
 
 
-def test_iterate_c3_small_mixed_noise():
+@pytest.mark.parametrize("path", PATHS)
+def test_iterate_c3_small_mixed_noise(path):
     """per-pixel W (A21), P = 63, 2x4 facets."""
     pb = synth.make_config(3, n=1024, overlap=64)
-    check_pair(run_pair(pb, 10))
+    check_pair(run_pair(pb, 10, path))
 
 
 def test_default_tau_matches_oracle():
