@@ -54,7 +54,7 @@ OP_CASES = [
 PATHS = [D.CONV_DIRECT, D.CONV_FFT]
 
 
-@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("path", PATHS, ids=["direct", "fft"])
 @pytest.mark.parametrize("k,n,facets,O", OP_CASES)
 def test_apply_H_HT_parity(k, n, facets, O, path):
     pb = synth.make_config(k, n=n, facets=facets, overlap=O)
@@ -68,7 +68,7 @@ def test_apply_H_HT_parity(k, n, facets, O, path):
     assert rel_l2(g, op.HT(r)) <= H_TOL
 
 
-@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("path", PATHS, ids=["direct", "fft"])
 @pytest.mark.parametrize("P,G,shape", [(1, 2, (37, 45)), (3, 1, (20, 300)), (7, 3, (131, 259)),
                                        (15, 2, (256, 129)), (127, 4, (400, 300)), (63, 3, (700, 1100))])
 def test_apply_parity_odd_shapes(P, G, shape, path):
@@ -118,7 +118,7 @@ def test_gpu_identical_and_delta_psfs():
         assert rel_l2(dev.apply_H(x), x[c:n - c, c:n - c]) <= 1e-6
 
 
-@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("path", PATHS, ids=["direct", "fft"])
 @pytest.mark.parametrize("k,count", [(3, 4000), (4, 3000)])
 def test_apply_full_size_sampled(k, count, path):
     """BASELINE full sizes (c3 4096^2, c4 16384^2), bench launch configuration,
@@ -170,26 +170,26 @@ def check_pair(res):
     assert res["x"][0].min() >= 0.0
 
 
-@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("path", PATHS, ids=["direct", "fft"])
 def test_iterate_c1_full(path):
     pb = synth.make_config(1)
     check_pair(run_pair(pb, pb.iters, path))
 
 
-@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("path", PATHS, ids=["direct", "fft"])
 def test_iterate_c2_full(path):
     pb = synth.make_config(2)
     check_pair(run_pair(pb, pb.iters, path))
 
 
-@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("path", PATHS, ids=["direct", "fft"])
 @pytest.mark.parametrize("over", [dict(inner_steps=2), dict(reg_kind=1), dict(tv_boundary=1)])
 def test_iterate_variants_ragged(over, path):
     pb = synth.make_config(2, n=300, facets=(3, 2), overlap=40)
     check_pair(run_pair(pb, 15, path, **over))
 
 
-@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("path", PATHS, ids=["direct", "fft"])
 def test_iterate_c3_small_mixed_noise(path):
     """per-pixel W (A21), P = 63, 2x4 facets."""
     pb = synth.make_config(3, n=1024, overlap=64)
