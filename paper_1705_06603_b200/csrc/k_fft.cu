@@ -33,6 +33,7 @@ namespace deblur {
 namespace {
 
 constexpr int NT = 256;
+constexpr int INV_HT = 3;   // k_rows_inv mode for H^T (H modes are FftMode values)
 
 struct FftArgs {
     const FacetDev *facets;
@@ -406,7 +407,7 @@ __global__ void __launch_bounds__(NT) k_rows_inv(FftArgs A, int mode) {
     const float2 *base = A.scratch + (int64_t)tile * A.tile_rows * G::LDF;
     const float scale = A.scale;
 
-    if (mode != 1) {
+    if (mode != INV_HT) {
         const float2 *O = base + ((int64_t)A.NQ * S + r0) * G::LDF;
         c2r_rows<S>(O, G::LDF, nrows, a, b, outs, A.W);
         double dsum = 0.0;
@@ -699,7 +700,7 @@ cudaError_t fft_HT(FftPlan &f, const FacetDev *d_facets, cudaStream_t s) {
     cudaError_t e;
     if ((e = do_rows_fwd(f.S, a, n, 1, 0, nullptr, 0, nullptr, s)) != cudaSuccess) return e;
     if ((e = do_cols(f.S, a, n, 1, nullptr, nullptr, 0, s)) != cudaSuccess) return e;
-    return do_rows_inv(f.S, a, n, f.T, 1, s);
+    return do_rows_inv(f.S, a, n, f.T, INV_HT, s);
 }
 
 cudaError_t fft_data_partials(FftPlan &f, std::vector<double> &out) {
