@@ -32,7 +32,6 @@ namespace deblur {
 
 namespace {
 
-constexpr int NT = 256;
 constexpr int INV_HT = 3;   // k_rows_inv mode for H^T (H modes are FftMode values)
 
 struct FftArgs {
@@ -59,7 +58,7 @@ __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
 
-// multiply by -i*SIGN... : rot(v) = v * (SIGN < 0 ? -i : +i)
+// v * (SIGN < 0 ? -i : +i)
 template <int SIGN>
 __device__ __forceinline__ float2 rot90(float2 v) {
     return SIGN < 0 ? make_float2(v.y, -v.x) : make_float2(-v.y, v.x);
@@ -67,16 +66,16 @@ __device__ __forceinline__ float2 rot90(float2 v) {
 
 template <int SIGN>
 __device__ __forceinline__ void dft2(float2 &a, float2 &b) {
-    float2 t = a;
+    const float2 t = a;
     a = cadd(t, b);
     b = csub(t, b);
 }
 
+// X_k = sum_n a_n e^{SIGN 2 pi i n k / 4}
 template <int SIGN>
 __device__ __forceinline__ void dft4(float2 &a0, float2 &a1, float2 &a2, float2 &a3) {
-    // X_k = sum_n a_n e^{SIGN 2 pi i n k / 4}
-    float2 s0 = cadd(a0, a2), d0 = csub(a0, a2);
-    float2 s1 = cadd(a1, a3), d1 = rot90<SIGN>(csub(a1, a3));
+    const float2 s0 = cadd(a0, a2), d0 = csub(a0, a2);
+    const float2 s1 = cadd(a1, a3), d1 = rot90<SIGN>(csub(a1, a3));
     a0 = cadd(s0, s1);
     a2 = csub(s0, s1);
     a1 = cadd(d0, d1);
@@ -84,373 +83,527 @@ __device__ __forceinline__ void dft4(float2 &a0, float2 &a1, float2 &a2, float2 
 }
 
 template <int SIGN>
-__device__ __forceinline__ void dft8(float2 (&v)[8]) {
+__device__ __forceinline__ void dft8(float2 &v0, float2 &v1, float2 &v2, float2 &v3, float2 &v4, float2 &v5,
+                                     float2 &v6, float2 &v7) {
     const float r = 0.70710678118654752f;
-    // even/odd split: X_k = E_k + w8^k O_k, X_{k+4} = E_k - w8^k O_k
-    float2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
-    float2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+    float2 e0 = v0, e1 = v2, e2 = v4, e3 = v6;
+    float2 o0 = v1, o1 = v3, o2 = v5, o3 = v7;
     dft4<SIGN>(e0, e1, e2, e3);
     dft4<SIGN>(o0, o1, o2, o3);
     // w8^1 = (r, SIGN r), w8^2 = SIGN i, w8^3 = (-r, SIGN r)
     const float2 t1 = make_float2(r * (o1.x - SIGN * o1.y), r * (o1.y + SIGN * o1.x));
     const float2 t2 = rot90<SIGN>(o2);
     const float2 t3 = make_float2(-r * (o3.x + SIGN * o3.y), r * (SIGN * o3.x - o3.y));
-    v[0] = cadd(e0, o0); v[4] = csub(e0, o0);
-    v[1] = cadd(e1, t1); v[5] = csub(e1, t1);
-    v[2] = cadd(e2, t2); v[6] = csub(e2, t2);
-    v[3] = cadd(e3, t3); v[7] = csub(e3, t3);
+    v0 = cadd(e0, o0); v4 = csub(e0, o0);
+    v1 = cadd(e1, t1); v5 = csub(e1, t1);
+    v2 = cadd(e2, t2); v6 = csub(e2, t2);
+    v3 = cadd(e3, t3); v7 = csub(e3, t3);
 }
 
-// One Stockham stage (Govindaraju et al. formulation) over nb transforms of length L
-// stored at in[t*stride + n]; twiddles W[idx * wmul] with W the size-S table.
-template <int R, int SIGN>
-__device__ __forceinline__ void stage(const float2 *__restrict__ in, float2 *__restrict__ out, int L, int Ns, int nb,
-                                      int stride, const float2 *__restrict__ W, int wmul, int S) {
-    const int LR = L / R;
-    const int total = nb * LR;
-    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-        const int t = idx / LR, j = idx - t * LR;
-        const float2 *src = in + (int64_t)t * stride;
-        float2 *dst = out + (int64_t)t * stride;
-        float2 v[8];
-#pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = src[j + r * LR];
-        const int k = j % Ns;
+// Radix plans.  For L >= 64 the first and the last stage are radix 8, so the
+// elements a thread produces in the last stage of one transform are exactly the
+// ones it consumes in the first stage of the next (accumulators stay in registers).
+__host__ __device__ constexpr int fft_nst(int L) {
+    return L == 16 ? 2 : L == 32 ? 2 : L == 64 ? 2 : L == 128 ? 3 : L == 256 ? 3 : L == 512 ? 3 : L == 1024 ? 4 : 0;
+}
+__host__ __device__ constexpr int fft_rad(int L, int s) {
+    return L == 16 ? 4
+         : L == 32 ? (s == 0 ? 8 : 4)
+         : L == 64 ? 8
+         : L == 128 ? (s == 1 ? 2 : 8)
+         : L == 256 ? (s == 1 ? 4 : 8)
+         : L == 512 ? 8
+         : ((s == 1 || s == 2) ? 4 : 8);
+}
+__host__ __device__ constexpr int fft_ns(int L, int s) { return s == 0 ? 1 : fft_ns(L, s - 1) * fft_rad(L, s - 1); }
+
+// One Stockham stage of NB batched length-L transforms at buf[t*STRIDE + n] executed
+// by NTH threads; butterfly b = tid + NTH*i maps to transform t = b % NB
+// (transform-fastest: a half-warp touches 16 transforms at one position, which
+// the padded STRIDE spreads over distinct banks) and butterfly j = b / NB.
+template <int L, int NB, int STRIDE, int NTH, int s>
+struct Stage {
+    static constexpr int R = fft_rad(L, s), Ns = fft_ns(L, s), LR = L / R;
+    static constexpr int E = NB * L / NTH, BPT = E / R;
+    static_assert(E % R == 0, "elements per thread must be a multiple of the radix");
+    __device__ static __forceinline__ void bj(int i, int tid, int &t, int &j) {
+        const int b = tid + NTH * i;
+        t = b % NB;
+        j = b / NB;
+    }
+    __device__ static __forceinline__ int in_n(int j, int r) { return j + r * LR; }
+    __device__ static __forceinline__ int out_n(int j, int r) { return (j / Ns) * Ns * R + (j % Ns) + r * Ns; }
+    template <int SIGN>
+    __device__ static __forceinline__ void bfly(float2 *v, int j, const float2 *W, int S) {
         if (Ns > 1) {
-            const int base = k * (L / (Ns * R));
+            const int k = j % Ns;
+            const int step = S / (Ns * R);
 #pragma unroll
             for (int r = 1; r < R; ++r) {
-                float2 w = __ldg(W + ((base * r * wmul) & (S - 1)));
+                float2 w = W[(k * r * step) & (S - 1)];
                 if (SIGN > 0) w.y = -w.y;
                 v[r] = cmul(v[r], w);
             }
         }
-        if (R == 8) {
-            dft8<SIGN>(v);
-        } else if (R == 4) {
-            dft4<SIGN>(v[0], v[1], v[2], v[3]);
-        } else {
-            dft2<SIGN>(v[0], v[1]);
-        }
-        const int idxD = (j / Ns) * Ns * R + k;
+        if (R == 8) dft8<SIGN>(v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7]);
+        else if (R == 4) dft4<SIGN>(v[0], v[1], v[2], v[3]);
+        else dft2<SIGN>(v[0], v[1]);
+    }
+    template <int SIGN>
+    __device__ static __forceinline__ void load_bfly(const float2 *buf, float2 (&v)[E], int tid, const float2 *W, int S) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) dst[idxD + r * Ns] = v[r];
+        for (int i = 0; i < BPT; ++i) {
+            int t, j;
+            bj(i, tid, t, j);
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[i * R + r] = buf[t * STRIDE + in_n(j, r)];
+            bfly<SIGN>(&v[i * R], j, W, S);
+        }
     }
-}
+    __device__ static __forceinline__ void store(float2 *buf, const float2 (&v)[E], int tid) {
+#pragma unroll
+        for (int i = 0; i < BPT; ++i) {
+            int t, j;
+            bj(i, tid, t, j);
+#pragma unroll
+            for (int r = 0; r < R; ++r) buf[t * STRIDE + out_n(j, r)] = v[i * R + r];
+        }
+    }
+};
 
-// In-smem FFT of nb transforms of length L (power of 2).  Data starts in a; the
-// result pointer (a or b) is returned.  All threads of the CTA participate; ends
-// with __syncthreads().  SIGN = -1 forward, +1 inverse (unnormalised).
-template <int SIGN>
-__device__ float2 *fft_smem(float2 *a, float2 *b, int L, int nb, int stride, const float2 *W, int S) {
-    const int wmul = S / L;
-    int Ns = 1;
-    while (Ns < L) {
-        const int R = (L / Ns >= 8) ? 8 : (L / Ns);
-        if (R == 8) stage<8, SIGN>(a, b, L, Ns, nb, stride, W, wmul, S);
-        else if (R == 4) stage<4, SIGN>(a, b, L, Ns, nb, stride, W, wmul, S);
-        else stage<2, SIGN>(a, b, L, Ns, nb, stride, W, wmul, S);
+// stages 1 .. NS-1 with exchanges through `work`; v holds stage-0 outputs on entry
+// and last-stage outputs on exit.  Contains the barriers it needs.
+template <int L, int NB, int STRIDE, int NTH, int SIGN, int s, int NS>
+struct Mid {
+    static constexpr int E = NB * L / NTH;
+    __device__ static __forceinline__ void run(float2 *work, float2 (&v)[E], int tid, const float2 *W, int S) {
+        Stage<L, NB, STRIDE, NTH, s - 1>::store(work, v, tid);
         __syncthreads();
-        float2 *t = a; a = b; b = t;
-        Ns *= R;
+        Stage<L, NB, STRIDE, NTH, s>::template load_bfly<SIGN>(work, v, tid, W, S);
+        __syncthreads();
+        Mid<L, NB, STRIDE, NTH, SIGN, s + 1, NS>::run(work, v, tid, W, S);
     }
-    return a;
-}
+};
+template <int L, int NB, int STRIDE, int NTH, int SIGN, int NS>
+struct Mid<L, NB, STRIDE, NTH, SIGN, NS, NS> {
+    static constexpr int E = NB * L / NTH;
+    __device__ static __forceinline__ void run(float2 *, float2 (&)[E], int, const float2 *, int) {}
+};
 
+template <int L, int NB, int STRIDE, int NTH>
+struct Fft {
+    static constexpr int NS = fft_nst(L);
+    static constexpr int E = NB * L / NTH;
+    using First = Stage<L, NB, STRIDE, NTH, 0>;
+    using Last = Stage<L, NB, STRIDE, NTH, NS - 1>;
+    template <int SIGN>
+    __device__ static __forceinline__ void middle(float2 *work, float2 (&v)[E], int tid, const float2 *W, int S) {
+        Mid<L, NB, STRIDE, NTH, SIGN, 1, NS>::run(work, v, tid, W, S);
+    }
+};
+
+// geometry of the row passes (length SH complex transforms, NBR rows per CTA)
 template <int S>
-struct Geo {
-    static constexpr int SH = S / 2;
-    static constexpr int NF = SH + 1;
-    static constexpr int LDF = SH + 16;            // padded row length of spectra
-    static constexpr int ROWS = (S >= 512) ? 8 : 16;  // rows per CTA in the row passes
-    static constexpr int C = (S >= 1024) ? 4 : 8;   // columns per CTA in the column pass
-    static constexpr int CS = S + 1;                // smem column stride (bank spread)
-    static constexpr int RS = SH + 1;               // smem row stride in the row passes
+struct GR {
+    static constexpr int SH = S / 2, NF = SH + 1;
+    static constexpr int NTH = 256;
+    static constexpr int NB = (S <= 64) ? 64 : (S <= 128) ? 32 : 16;
+    static constexpr int RS = SH + 1;    // smem row stride (float2): transform-fastest access is conflict-free
+    static constexpr int XS = S + 2;     // smem real-row stride (floats)
+    using F = Fft<SH, NB, RS, NTH>;
+    static constexpr int E = F::E;
+};
+// geometry of the column pass (length S complex transforms, NBC columns per CTA)
+template <int S>
+struct GC {
+    static constexpr int NTH = 512;
+    static constexpr int NB = (S <= 64) ? 64 : (S <= 128) ? 32 : (S <= 512) ? 16 : 8;
+    static constexpr int CS = S + ((NB >= 16) ? 1 : 16 / NB);
+    using F = Fft<S, NB, CS, NTH>;
+    static constexpr int E = F::E;
+};
+template <int S>
+struct LD {
+    static constexpr int LDF = S / 2 + GC<S>::NB;   // padded spectrum row length (float2)
 };
 
 // ------------------------------------------------------------------ pass A / A'
-// mode 0: H (x window . wx_q, one R2C per active q); mode 1: H^T (r window); mode 2: PSF spectra
+// mode 0: H (x window . wx_q, one R2C per active q); 1: H^T (r window); 2: PSF spectra rows
 template <int S>
-__global__ void __launch_bounds__(NT) k_rows_fwd(FftArgs A, int mode, int par, const float *psfs, int npsf,
-                                                 float2 *hrows) {
-    using G = Geo<S>;
+__global__ void __launch_bounds__(256) k_rows_fwd(FftArgs A, int mode, int par, const float *psfs, int npsf,
+                                                  float2 *hrows) {
+    using G = GR<S>;
+    using F = typename G::F;
+    constexpr int NB = G::NB, SH = G::SH, NF = G::NF, RS = G::RS, XS = G::XS, LDF = LD<S>::LDF;
     extern __shared__ __align__(16) float2 sm2[];
-    float *xs = reinterpret_cast<float *>(sm2);                  // ROWS x S reals
-    float2 *a = sm2 + G::ROWS * S / 2;                           // ROWS x RS
-    float2 *b = a + G::ROWS * G::RS;
-    const int nblk = S / G::ROWS;
-    const int tile = blockIdx.x / nblk, r0 = (blockIdx.x % nblk) * G::ROWS;
+    float2 *Wsm = sm2;                                      // S
+    float2 *work = Wsm + S;                                 // NB x RS
+    float *xs = reinterpret_cast<float *>(work + NB * RS);  // NB x XS
+    float *wxs = xs + NB * XS;                              // S
+    const int tid = threadIdx.x;
+    const int nblk = S / NB;
+    const int tile = blockIdx.x / nblk, r0 = (blockIdx.x % nblk) * NB;
     const int P = A.P, c2 = P - 1;
     int nq = 1, q0 = 0;
     TileDesc t{};
-    const FacetDev *F = nullptr;
+    const FacetDev *Fd = nullptr;
     if (mode == 2) {
         if (tile >= npsf) return;
     } else {
         t = A.tiles[tile];
-        F = &A.facets[t.f];
+        Fd = &A.facets[t.f];
         if (mode == 0) { q0 = t.q0; nq = t.q1 - t.q0 + 1; }
     }
-    // load the real rows
-    for (int idx = threadIdx.x; idx < G::ROWS * S; idx += NT) {
+    for (int i = tid; i < S; i += G::NTH) Wsm[i] = A.W[i];
+    for (int idx = tid; idx < NB * S; idx += G::NTH) {
         const int rr = idx / S, cc = idx - rr * S;
         const int row = r0 + rr;
         float v = 0.f;
         if (mode == 0) {
             const int ly = t.y0 + row, lx = t.x0 + cc;
-            if (ly < F->ny && lx < F->nx) v = F->x[par][(int64_t)ly * F->ep + lx];
+            if (ly < Fd->ny && lx < Fd->nx) v = Fd->x[par][(int64_t)ly * Fd->ep + lx];
         } else if (mode == 1) {
             const int ri = t.y0 - c2 + row, rj = t.x0 - c2 + cc;
-            if (ri >= 0 && ri < F->my && rj >= 0 && rj < F->mx) v = F->r[(int64_t)ri * F->op + rj];
+            if (ri >= 0 && ri < Fd->my && rj >= 0 && rj < Fd->mx) v = Fd->r[(int64_t)ri * Fd->op + rj];
         } else {
             if (row < P && cc < P) v = psfs[(int64_t)tile * P * P + row * P + cc];
         }
-        xs[idx] = v;
+        xs[rr * XS + cc] = v;
     }
-    __syncthreads();
     for (int qi = 0; qi < nq; ++qi) {
-        const float *wxq = (mode == 0) ? A.wx + (size_t)(q0 + qi) * A.Nx + F->ex0 + t.x0 : nullptr;
-        for (int idx = threadIdx.x; idx < G::ROWS * G::SH; idx += NT) {
-            const int rr = idx / G::SH, n = idx - rr * G::SH;
-            float e = xs[rr * S + 2 * n], o = xs[rr * S + 2 * n + 1];
-            if (mode == 0) {
-                const int lx = t.x0 + 2 * n;
-                e *= (lx < F->nx) ? __ldg(wxq + 2 * n) : 0.f;
-                o *= (lx + 1 < F->nx) ? __ldg(wxq + 2 * n + 1) : 0.f;
-            }
-            a[rr * G::RS + n] = make_float2(e, o);
+        if (mode == 0) {
+            __syncthreads();
+            const float *wxq = A.wx + (size_t)(q0 + qi) * A.Nx + Fd->ex0 + t.x0;
+            for (int i = tid; i < S; i += G::NTH) wxs[i] = (t.x0 + i < Fd->nx) ? __ldg(wxq + i) : 0.f;
         }
         __syncthreads();
-        float2 *Z = fft_smem<-1>(a, b, G::SH, G::ROWS, G::RS, A.W, S);
+        // stage 0 straight from the real rows: z[n] = (x[2n] w[2n], x[2n+1] w[2n+1])
+        float2 v[G::E];
+        using S0 = typename F::First;
+#pragma unroll
+        for (int i = 0; i < S0::BPT; ++i) {
+            int tt, j;
+            S0::bj(i, tid, tt, j);
+#pragma unroll
+            for (int r = 0; r < S0::R; ++r) {
+                const int n = S0::in_n(j, r);
+                float2 z = *reinterpret_cast<const float2 *>(xs + tt * XS + 2 * n);
+                if (mode == 0) {
+                    const float2 w = *reinterpret_cast<const float2 *>(wxs + 2 * n);
+                    z.x *= w.x;
+                    z.y *= w.y;
+                }
+                v[i * S0::R + r] = z;
+            }
+            S0::template bfly<-1>(&v[i * S0::R], j, Wsm, S);
+        }
+        __syncthreads();      // Wsm/xs readers done before work is written (work is disjoint; keeps phases clean)
+        F::template middle<-1>(work, v, tid, Wsm, S);
+        F::Last::store(work, v, tid);
+        __syncthreads();
         // R2C post-processing: X[k] = (Zk + conj Z_{SH-k})/2 - i/2 W_S^k (Zk - conj Z_{SH-k})
-        for (int idx = threadIdx.x; idx < G::ROWS * G::NF; idx += NT) {
-            const int rr = idx / G::NF, k = idx - rr * G::NF;
-            const float2 zk = Z[rr * G::RS + (k & (G::SH - 1))];
-            const float2 zc = conjf2(Z[rr * G::RS + ((G::SH - k) & (G::SH - 1))]);
-            const float2 s = make_float2(0.5f * (zk.x + zc.x), 0.5f * (zk.y + zc.y));
+        for (int idx = tid; idx < NB * NF; idx += G::NTH) {
+            const int rr = idx / NF, k = idx - rr * NF;
+            const float2 zk = work[rr * RS + (k & (SH - 1))];
+            const float2 zc = conjf2(work[rr * RS + ((SH - k) & (SH - 1))]);
+            const float2 sh = make_float2(0.5f * (zk.x + zc.x), 0.5f * (zk.y + zc.y));
             const float2 d = make_float2(0.5f * (zk.x - zc.x), 0.5f * (zk.y - zc.y));
-            const float2 w = __ldg(A.W + (k & (S - 1)));
-            const float2 wd = cmul(w, d);                 // W^k d
-            const float2 X = make_float2(s.x + wd.y, s.y - wd.x);   // s - i W^k d
+            const float2 wd = cmul(Wsm[k & (S - 1)], d);
+            const float2 X = make_float2(sh.x + wd.y, sh.y - wd.x);
             float2 *dst;
             if (mode == 2)
-                dst = hrows + ((int64_t)tile * S + r0 + rr) * G::LDF;
+                dst = hrows + ((int64_t)tile * S + r0 + rr) * LDF;
             else
-                dst = A.scratch + (int64_t)tile * A.tile_rows * G::LDF + ((int64_t)qi * S + r0 + rr) * G::LDF;
+                dst = A.scratch + (int64_t)tile * A.tile_rows * LDF + ((int64_t)qi * S + r0 + rr) * LDF;
             dst[k] = X;
         }
-        __syncthreads();
     }
 }
 
 // ------------------------------------------------------------------ pass B / B'
-// mode 0: H; mode 1: H^T; mode 2: PSF spectra (forward column DFT of hrows -> Hhat)
+// mode 0: H; 1: H^T; 2: PSF spectra (forward column DFT of hrows -> Hhat)
 template <int S>
-__global__ void __launch_bounds__(NT) k_cols(FftArgs A, int mode, const float2 *hrows, float2 *hhat, int npsf) {
-    using G = Geo<S>;
+__global__ void __launch_bounds__(512) k_cols(FftArgs A, int mode, const float2 *hrows, float2 *hhat, int npsf) {
+    using G = GC<S>;
+    using F = typename G::F;
+    constexpr int NB = G::NB, CS = G::CS, E = G::E, LDF = LD<S>::LDF, NF = S / 2 + 1;
+    using S0 = typename F::First;
+    using SL = typename F::Last;
+    static_assert(S0::R == SL::R, "first/last radix must match");
     extern __shared__ __align__(16) float2 sm2[];
-    constexpr int C = G::C, CS = G::CS;
-    float2 *colq = sm2;               // C x CS : A_q columns (H) / R-hat (H^T)
-    float2 *w0 = colq + C * CS;       // work (ping)
-    float2 *w1 = w0 + C * CS;         // work (pong)
-    float2 *acc = w1 + C * CS;        // accumulator
-    const int nchunk = (G::NF + C - 1) / C;
-    const int tile = blockIdx.x / nchunk, f0 = (blockIdx.x % nchunk) * C;
+    float2 *Wsm = sm2;               // S
+    float2 *colq = Wsm + S;          // NB x CS
+    float2 *work = colq + NB * CS;   // NB x CS
+    float *wys = reinterpret_cast<float *>(work + NB * CS);   // S
+    const int tid = threadIdx.x;
+    const int nchunk = (NF + NB - 1) / NB;
+    const int tile = blockIdx.x / nchunk, f0 = (blockIdx.x % nchunk) * NB;
     const int P = A.P, c2 = P - 1, T = S - P + 1;
+    for (int i = tid; i < S; i += G::NTH) Wsm[i] = A.W[i];
+    __syncthreads();
+    float2 v[E];
 
     if (mode == 2) {
         if (tile >= npsf) return;
-        for (int idx = threadIdx.x; idx < C * S; idx += NT) {
-            const int c = idx % C, ky = idx / C;
-            w0[c * CS + ky] = (f0 + c < G::NF) ? hrows[((int64_t)tile * S + ky) * G::LDF + f0 + c] : make_float2(0, 0);
+        const float2 *src = hrows + (int64_t)tile * S * LDF + f0;
+#pragma unroll
+        for (int i = 0; i < S0::BPT; ++i) {
+            int t, j;
+            S0::bj(i, tid, t, j);
+#pragma unroll
+            for (int r = 0; r < S0::R; ++r) v[i * S0::R + r] = src[(int64_t)S0::in_n(j, r) * LDF + t];
+            S0::template bfly<-1>(&v[i * S0::R], j, Wsm, S);
         }
-        __syncthreads();
-        float2 *Z = fft_smem<-1>(w0, w1, S, C, CS, A.W, S);
-        for (int idx = threadIdx.x; idx < C * S; idx += NT) {
-            const int c = idx % C, ky = idx / C;
-            if (f0 + c < G::NF) hhat[((int64_t)tile * S + ky) * G::LDF + f0 + c] = Z[c * CS + ky];
+        F::template middle<-1>(work, v, tid, Wsm, S);
+        float2 *dst = hhat + (int64_t)tile * S * LDF + f0;
+#pragma unroll
+        for (int i = 0; i < SL::BPT; ++i) {
+            int t, j;
+            SL::bj(i, tid, t, j);
+#pragma unroll
+            for (int r = 0; r < SL::R; ++r) dst[(int64_t)SL::out_n(j, r) * LDF + t] = v[i * SL::R + r];
         }
         return;
     }
 
-    const TileDesc t = A.tiles[tile];
-    const FacetDev &F = A.facets[t.f];
-    float2 *base = A.scratch + (int64_t)tile * A.tile_rows * G::LDF;
+    const TileDesc td = A.tiles[tile];
+    const FacetDev &Fd = A.facets[td.f];
+    float2 *base = A.scratch + (int64_t)tile * A.tile_rows * LDF;
 
     if (mode == 0) {
-        for (int idx = threadIdx.x; idx < C * S; idx += NT) acc[(idx % C) * CS + idx / C] = make_float2(0, 0);
-        for (int q = t.q0; q <= t.q1; ++q) {
+        float2 acc[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[e] = make_float2(0.f, 0.f);
+        for (int q = td.q0; q <= td.q1; ++q) {
             __syncthreads();
-            const float2 *Aq = base + (int64_t)(q - t.q0) * S * G::LDF;
-            for (int idx = threadIdx.x; idx < C * S; idx += NT) {
-                const int c = idx % C, row = idx / C;
-                colq[c * CS + row] = Aq[(int64_t)row * G::LDF + f0 + c];
+            const float2 *Aq = base + (int64_t)(q - td.q0) * S * LDF + f0;
+            for (int idx = tid; idx < NB * S; idx += G::NTH) {
+                const int c = idx % NB, row = idx / NB;
+                colq[c * CS + row] = Aq[(int64_t)row * LDF + c];
             }
-            for (int p = t.p0; p <= t.p1; ++p) {
+            for (int p = td.p0; p <= td.p1; ++p) {
                 __syncthreads();
-                const float *wyp = A.wy + (size_t)p * A.Ny + F.ey0 + t.y0;
-                for (int idx = threadIdx.x; idx < C * S; idx += NT) {
-                    const int c = idx % C, row = idx / C;
-                    const float wv = (t.y0 + row < F.ny) ? __ldg(wyp + row) : 0.f;
-                    const float2 v = colq[c * CS + row];
-                    w0[c * CS + row] = make_float2(wv * v.x, wv * v.y);
+                const float *wyp = A.wy + (size_t)p * A.Ny + Fd.ey0 + td.y0;
+                for (int i = tid; i < S; i += G::NTH) wys[i] = (td.y0 + i < Fd.ny) ? __ldg(wyp + i) : 0.f;
+                __syncthreads();
+                // stage 0 from colq, weighted by the row weight wy_p (constant along the row)
+#pragma unroll
+                for (int i = 0; i < S0::BPT; ++i) {
+                    int t, j;
+                    S0::bj(i, tid, t, j);
+#pragma unroll
+                    for (int r = 0; r < S0::R; ++r) {
+                        const int n = S0::in_n(j, r);
+                        const float2 c = colq[t * CS + n];
+                        const float wv = wys[n];
+                        v[i * S0::R + r] = make_float2(wv * c.x, wv * c.y);
+                    }
+                    S0::template bfly<-1>(&v[i * S0::R], j, Wsm, S);
                 }
-                __syncthreads();
-                float2 *Z = fft_smem<-1>(w0, w1, S, C, CS, A.W, S);
+                F::template middle<-1>(work, v, tid, Wsm, S);
                 const int slot = A.psf_slot[p * A.Gx + q];
-                const float2 *Hk = A.Hhat + (int64_t)slot * S * G::LDF;
-                for (int idx = threadIdx.x; idx < C * S; idx += NT) {
-                    const int c = idx % C, ky = idx / C;
-                    const float2 h = __ldg(Hk + (int64_t)ky * G::LDF + f0 + c);
-                    float2 &o = acc[c * CS + ky];
-                    o = cadd(o, cmul(Z[c * CS + ky], h));
+                const float2 *Hk = A.Hhat + (int64_t)slot * S * LDF + f0;
+#pragma unroll
+                for (int i = 0; i < SL::BPT; ++i) {
+                    int t, j;
+                    SL::bj(i, tid, t, j);
+#pragma unroll
+                    for (int r = 0; r < SL::R; ++r) {
+                        const float2 h = __ldg(Hk + (int64_t)SL::out_n(j, r) * LDF + t);
+                        acc[i * SL::R + r] = cadd(acc[i * SL::R + r], cmul(v[i * SL::R + r], h));
+                    }
                 }
             }
         }
+        // inverse DFT along y; the accumulators already sit at stage-0 input positions
+#pragma unroll
+        for (int i = 0; i < S0::BPT; ++i) {
+            int t, j;
+            S0::bj(i, tid, t, j);
+            S0::template bfly<+1>(&acc[i * S0::R], j, Wsm, S);
+        }
         __syncthreads();
-        // inverse DFT along y of the accumulated spectrum (acc, w0 as pong)
-        float2 *z = fft_smem<+1>(acc, w0, S, C, CS, A.W, S);
-        float2 *O = base + (int64_t)A.NQ * S * G::LDF;
-        for (int idx = threadIdx.x; idx < C * T; idx += NT) {
-            const int c = idx % C, rr = idx / C;
-            if (f0 + c < G::NF) O[(int64_t)rr * G::LDF + f0 + c] = z[c * CS + c2 + rr];
+        F::template middle<+1>(work, acc, tid, Wsm, S);
+        float2 *O = base + (int64_t)A.NQ * S * LDF + f0;
+#pragma unroll
+        for (int i = 0; i < SL::BPT; ++i) {
+            int t, j;
+            SL::bj(i, tid, t, j);
+#pragma unroll
+            for (int r = 0; r < SL::R; ++r) {
+                const int n = SL::out_n(j, r);
+                if (n >= c2) O[(int64_t)(n - c2) * LDF + t] = acc[i * SL::R + r];
+            }
         }
         return;
     }
 
-    // mode 1 (H^T)
-    for (int idx = threadIdx.x; idx < C * S; idx += NT) {
-        const int c = idx % C, row = idx / C;
-        w0[c * CS + row] = base[(int64_t)row * G::LDF + f0 + c];
+    // mode 1 (H^T): R-hat = DFT_y of the r-window spectrum rows, kept in colq
+#pragma unroll
+    for (int i = 0; i < S0::BPT; ++i) {
+        int t, j;
+        S0::bj(i, tid, t, j);
+#pragma unroll
+        for (int r = 0; r < S0::R; ++r) v[i * S0::R + r] = base[(int64_t)S0::in_n(j, r) * LDF + f0 + t];
+        S0::template bfly<-1>(&v[i * S0::R], j, Wsm, S);
     }
-    __syncthreads();
-    {
-        float2 *R = fft_smem<-1>(w0, w1, S, C, CS, A.W, S);
-        if (R != colq)
-            for (int idx = threadIdx.x; idx < C * CS; idx += NT) colq[idx] = R[idx];
-    }
-    float2 *Bbase = base + (int64_t)S * G::LDF;
-    for (int q = t.q0; q <= t.q1; ++q) {
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < C * S; idx += NT) acc[(idx % C) * CS + idx / C] = make_float2(0, 0);
-        for (int p = t.p0; p <= t.p1; ++p) {
+    F::template middle<-1>(work, v, tid, Wsm, S);
+    SL::store(colq, v, tid);
+    float2 *Bbase = base + (int64_t)S * LDF + f0;
+    for (int q = td.q0; q <= td.q1; ++q) {
+        float2 acc[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[e] = make_float2(0.f, 0.f);
+        for (int p = td.p0; p <= td.p1; ++p) {
+            __syncthreads();
+            const float *wyp = A.wy + (size_t)p * A.Ny + Fd.ey0 + td.y0;
+            for (int i = tid; i < S; i += G::NTH) wys[i] = (td.y0 + i < Fd.ny) ? __ldg(wyp + i) : 0.f;
             __syncthreads();
             const int slot = A.psf_slot[p * A.Gx + q];
-            const float2 *Hk = A.Hhat + (int64_t)slot * S * G::LDF;
-            for (int idx = threadIdx.x; idx < C * S; idx += NT) {
-                const int c = idx % C, ky = idx / C;
-                const float2 h = __ldg(Hk + (int64_t)ky * G::LDF + f0 + c);
-                w0[c * CS + ky] = cmulc(colq[c * CS + ky], h);
+            const float2 *Hk = A.Hhat + (int64_t)slot * S * LDF + f0;
+#pragma unroll
+            for (int i = 0; i < S0::BPT; ++i) {
+                int t, j;
+                S0::bj(i, tid, t, j);
+#pragma unroll
+                for (int r = 0; r < S0::R; ++r) {
+                    const int n = S0::in_n(j, r);
+                    v[i * S0::R + r] = cmulc(colq[t * CS + n], __ldg(Hk + (int64_t)n * LDF + t));
+                }
+                S0::template bfly<+1>(&v[i * S0::R], j, Wsm, S);
             }
-            __syncthreads();
-            float2 *z = fft_smem<+1>(w0, w1, S, C, CS, A.W, S);
-            const float *wyp = A.wy + (size_t)p * A.Ny + F.ey0 + t.y0;
-            for (int idx = threadIdx.x; idx < C * T; idx += NT) {
-                const int c = idx % C, rr = idx / C;
-                const float wv = (t.y0 + rr < F.ny) ? __ldg(wyp + rr) : 0.f;
-                const float2 v = z[c * CS + rr];
-                float2 &o = acc[c * CS + rr];
-                o = make_float2(o.x + wv * v.x, o.y + wv * v.y);
+            F::template middle<+1>(work, v, tid, Wsm, S);
+#pragma unroll
+            for (int i = 0; i < SL::BPT; ++i) {
+                int t, j;
+                SL::bj(i, tid, t, j);
+#pragma unroll
+                for (int r = 0; r < SL::R; ++r) {
+                    const int n = SL::out_n(j, r);
+                    const float wv = (n < T) ? wys[n] : 0.f;
+                    float2 &o = acc[i * SL::R + r];
+                    o = make_float2(o.x + wv * v[i * SL::R + r].x, o.y + wv * v[i * SL::R + r].y);
+                }
             }
         }
-        __syncthreads();
-        float2 *Bq = Bbase + (int64_t)(q - t.q0) * T * G::LDF;
-        for (int idx = threadIdx.x; idx < C * T; idx += NT) {
-            const int c = idx % C, rr = idx / C;
-            if (f0 + c < G::NF) Bq[(int64_t)rr * G::LDF + f0 + c] = acc[c * CS + rr];
+        float2 *Bq = Bbase + (int64_t)(q - td.q0) * T * LDF;
+#pragma unroll
+        for (int i = 0; i < SL::BPT; ++i) {
+            int t, j;
+            SL::bj(i, tid, t, j);
+#pragma unroll
+            for (int r = 0; r < SL::R; ++r) {
+                const int n = SL::out_n(j, r);
+                if (n < T) Bq[(int64_t)n * LDF + t] = acc[i * SL::R + r];
+            }
         }
     }
 }
 
 // ------------------------------------------------------------------ pass C / C'
-// C2R of one spectrum row X[0..SH] (global) into smem reals out[0..S) (unscaled: SH x)
+// C2R of NB spectrum rows (global, row stride LDF, rows >= nrows read as zero) into
+// smem reals outs[rr*XS + m] (unscaled: SH x the signal).
 template <int S>
-__device__ void c2r_rows(const float2 *__restrict__ src0, int64_t src_stride, int nrows, float2 *a, float2 *b,
-                         float *outs, const float2 *W) {
-    using G = Geo<S>;
-    for (int idx = threadIdx.x; idx < nrows * G::SH; idx += NT) {
-        const int rr = idx / G::SH, k = idx - rr * G::SH;
-        const float2 *X = src0 + rr * src_stride;
-        const float2 xk = X[k], xc = conjf2(X[G::SH - k]);
-        const float2 e = make_float2(0.5f * (xk.x + xc.x), 0.5f * (xk.y + xc.y));
-        const float2 d = make_float2(0.5f * (xk.x - xc.x), 0.5f * (xk.y - xc.y));
-        const float2 w = conjf2(__ldg(W + k));
-        const float2 o = cmul(d, w);                       // O_k
-        a[rr * G::RS + k] = make_float2(e.x - o.y, e.y + o.x);   // E + i O
+__device__ __forceinline__ void c2r_rows(const float2 *__restrict__ src0, int nrows, float2 *work, float *outs,
+                                         const float2 *Wsm) {
+    using G = GR<S>;
+    using F = typename G::F;
+    constexpr int NB = G::NB, SH = G::SH, RS = G::RS, XS = G::XS, LDF = LD<S>::LDF;
+    const int tid = threadIdx.x;
+    for (int idx = tid; idx < NB * SH; idx += G::NTH) {
+        const int rr = idx / SH, k = idx - rr * SH;
+        float2 zz = make_float2(0.f, 0.f);
+        if (rr < nrows) {
+            const float2 *X = src0 + (int64_t)rr * LDF;
+            const float2 xk = X[k], xc = conjf2(X[SH - k]);
+            const float2 e = make_float2(0.5f * (xk.x + xc.x), 0.5f * (xk.y + xc.y));
+            const float2 d = make_float2(0.5f * (xk.x - xc.x), 0.5f * (xk.y - xc.y));
+            const float2 o = cmul(d, conjf2(Wsm[k]));     // O_k
+            zz = make_float2(e.x - o.y, e.y + o.x);      // E + i O
+        }
+        work[rr * RS + k] = zz;
     }
     __syncthreads();
-    float2 *z = fft_smem<+1>(a, b, G::SH, nrows, G::RS, W, S);
-    for (int idx = threadIdx.x; idx < nrows * G::SH; idx += NT) {
-        const int rr = idx / G::SH, n = idx - rr * G::SH;
-        const float2 v = z[rr * G::RS + n];
-        outs[rr * S + 2 * n] = v.x;
-        outs[rr * S + 2 * n + 1] = v.y;
+    float2 v[G::E];
+    F::First::template load_bfly<+1>(work, v, tid, Wsm, S);
+    __syncthreads();
+    F::template middle<+1>(work, v, tid, Wsm, S);
+    using SL = typename F::Last;
+#pragma unroll
+    for (int i = 0; i < SL::BPT; ++i) {
+        int t, j;
+        SL::bj(i, tid, t, j);
+#pragma unroll
+        for (int r = 0; r < SL::R; ++r)
+            *reinterpret_cast<float2 *>(outs + t * XS + 2 * SL::out_n(j, r)) = v[i * SL::R + r];
     }
     __syncthreads();
 }
 
 template <int S>
-__global__ void __launch_bounds__(NT) k_rows_inv(FftArgs A, int mode) {
-    using G = Geo<S>;
+__global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
+    using G = GR<S>;
+    constexpr int NB = G::NB, RS = G::RS, XS = G::XS, LDF = LD<S>::LDF;
     extern __shared__ __align__(16) float2 sm2[];
-    float *outs = reinterpret_cast<float *>(sm2);            // ROWS x S reals
-    float2 *a = sm2 + G::ROWS * S / 2;
-    float2 *b = a + G::ROWS * G::RS;
-    float *gacc = reinterpret_cast<float *>(b + G::ROWS * G::RS);   // ROWS x T (H^T)
-    __shared__ double red[NT / 32];
+    float2 *Wsm = sm2;
+    float2 *work = Wsm + S;
+    float *outs = reinterpret_cast<float *>(work + NB * RS);   // NB x XS
+    float *gacc = outs + NB * XS;                              // NB x T (H^T)
+    __shared__ double red[256 / 32];
+    const int tid = threadIdx.x;
     const int P = A.P, c2 = P - 1, T = S - P + 1;
-    const int nblk = (T + G::ROWS - 1) / G::ROWS;
-    const int tile = blockIdx.x / nblk, r0 = (blockIdx.x % nblk) * G::ROWS;
-    const int nrows = min(G::ROWS, T - r0);
+    const int nblk = (T + NB - 1) / NB;
+    const int tile = blockIdx.x / nblk, r0 = (blockIdx.x % nblk) * NB;
+    const int nrows = min(NB, T - r0);
     const TileDesc t = A.tiles[tile];
-    const FacetDev &F = A.facets[t.f];
-    const float2 *base = A.scratch + (int64_t)tile * A.tile_rows * G::LDF;
+    const FacetDev &Fd = A.facets[t.f];
+    const float2 *base = A.scratch + (int64_t)tile * A.tile_rows * LDF;
     const float scale = A.scale;
+    for (int i = tid; i < S; i += G::NTH) Wsm[i] = A.W[i];
+    __syncthreads();
 
     if (mode != INV_HT) {
-        const float2 *O = base + ((int64_t)A.NQ * S + r0) * G::LDF;
-        c2r_rows<S>(O, G::LDF, nrows, a, b, outs, A.W);
+        c2r_rows<S>(base + ((int64_t)A.NQ * S + r0) * LDF, nrows, work, outs, Wsm);
         double dsum = 0.0;
-        for (int idx = threadIdx.x; idx < nrows * T; idx += NT) {
+        for (int idx = tid; idx < nrows * T; idx += G::NTH) {
             const int rr = idx / T, cc = idx - rr * T;
             const int oi = t.y0 + r0 + rr, oj = t.x0 + cc;
-            if (oi >= F.my || oj >= F.mx) continue;
-            const float hx = outs[rr * S + c2 + cc] * scale;
-            const int64_t o = (int64_t)oi * F.op + oj;
+            if (oi >= Fd.my || oj >= Fd.mx) continue;
+            const float hx = outs[rr * XS + c2 + cc] * scale;
+            const int64_t o = (int64_t)oi * Fd.op + oj;
             if (mode == FFT_PLAIN) {
-                F.r[o] = hx;
+                Fd.r[o] = hx;
             } else {
-                const float wv = F.w ? F.w[o] : F.w_scalar;
-                const float d = hx - F.y[o];
-                if (mode == FFT_RESIDUAL) F.r[o] = wv * d;
+                const float wv = Fd.w ? Fd.w[o] : Fd.w_scalar;
+                const float d = hx - Fd.y[o];
+                if (mode == FFT_RESIDUAL) Fd.r[o] = wv * d;
                 dsum += 0.5 * (double)wv * (double)d * (double)d;
             }
         }
         if (mode != FFT_PLAIN && A.partials) {
             const double s = block_sum(dsum, red);
-            if (threadIdx.x == 0) A.partials[blockIdx.x] = s;
+            if (tid == 0) A.partials[blockIdx.x] = s;
         }
         return;
     }
     // H^T: g = sum_q wx_q . C2R(B_q)
-    for (int idx = threadIdx.x; idx < nrows * T; idx += NT) gacc[idx] = 0.f;
-    const float2 *Bbase = base + (int64_t)S * G::LDF;
+    for (int idx = tid; idx < nrows * T; idx += G::NTH) gacc[idx] = 0.f;
+    const float2 *Bbase = base + (int64_t)S * LDF;
     for (int q = t.q0; q <= t.q1; ++q) {
         __syncthreads();
-        const float2 *Bq = Bbase + ((int64_t)(q - t.q0) * T + r0) * G::LDF;
-        c2r_rows<S>(Bq, G::LDF, nrows, a, b, outs, A.W);
-        const float *wxq = A.wx + (size_t)q * A.Nx + F.ex0 + t.x0;
-        for (int idx = threadIdx.x; idx < nrows * T; idx += NT) {
+        c2r_rows<S>(Bbase + ((int64_t)(q - t.q0) * T + r0) * LDF, nrows, work, outs, Wsm);
+        const float *wxq = A.wx + (size_t)q * A.Nx + Fd.ex0 + t.x0;
+        for (int idx = tid; idx < nrows * T; idx += G::NTH) {
             const int rr = idx / T, cc = idx - rr * T;
-            const float wv = (t.x0 + cc < F.nx) ? __ldg(wxq + cc) : 0.f;
-            gacc[idx] += wv * (outs[rr * S + cc] * scale);
+            const float wv = (t.x0 + cc < Fd.nx) ? __ldg(wxq + cc) : 0.f;
+            gacc[idx] += wv * (outs[rr * XS + cc] * scale);
         }
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < nrows * T; idx += NT) {
+    for (int idx = tid; idx < nrows * T; idx += G::NTH) {
         const int rr = idx / T, cc = idx - rr * T;
         const int fy = t.y0 + r0 + rr, fx = t.x0 + cc;
-        if (fy < F.ny && fx < F.nx) F.g[(int64_t)fy * F.ep + fx] = gacc[idx];
+        if (fy < Fd.ny && fx < Fd.nx) Fd.g[(int64_t)fy * Fd.ep + fx] = gacc[idx];
     }
 }
 
@@ -508,11 +661,17 @@ bool fft_prefer(int P) {
 }
 
 template <int S>
-static size_t smem_rows_fwd() { using G = Geo<S>; return (size_t)G::ROWS * S * 4 + 2 * (size_t)G::ROWS * G::RS * 8; }
+static size_t smem_rows_fwd() {
+    using G = GR<S>;
+    return (size_t)S * 8 + (size_t)G::NB * G::RS * 8 + (size_t)G::NB * G::XS * 4 + (size_t)S * 4;
+}
 template <int S>
-static size_t smem_cols() { using G = Geo<S>; return 4 * (size_t)G::C * G::CS * 8; }
+static size_t smem_cols() { using G = GC<S>; return (size_t)S * 8 + 2 * (size_t)G::NB * G::CS * 8 + (size_t)S * 4; }
 template <int S>
-static size_t smem_rows_inv(int T) { using G = Geo<S>; return (size_t)G::ROWS * S * 4 + 2 * (size_t)G::ROWS * G::RS * 8 + (size_t)G::ROWS * T * 4; }
+static size_t smem_rows_inv(int T) {
+    using G = GR<S>;
+    return (size_t)S * 8 + (size_t)G::NB * G::RS * 8 + (size_t)G::NB * G::XS * 4 + (size_t)G::NB * T * 4;
+}
 
 template <int S>
 static cudaError_t setup_attrs(int T) {
@@ -526,22 +685,22 @@ template <int S>
 static cudaError_t run_rows_fwd(const FftArgs &a, int ntiles, int mode, int par, const float *psfs, int npsf,
                                 float2 *hrows, cudaStream_t s) {
     if (ntiles == 0) return cudaSuccess;
-    k_rows_fwd<S><<<ntiles * (S / Geo<S>::ROWS), NT, smem_rows_fwd<S>(), s>>>(a, mode, par, psfs, npsf, hrows);
+    k_rows_fwd<S><<<ntiles * (S / GR<S>::NB), GR<S>::NTH, smem_rows_fwd<S>(), s>>>(a, mode, par, psfs, npsf, hrows);
     return cudaGetLastError();
 }
 template <int S>
 static cudaError_t run_cols(const FftArgs &a, int ntiles, int mode, const float2 *hrows, float2 *hhat, int npsf,
                             cudaStream_t s) {
     if (ntiles == 0) return cudaSuccess;
-    const int nchunk = (Geo<S>::NF + Geo<S>::C - 1) / Geo<S>::C;
-    k_cols<S><<<ntiles * nchunk, NT, smem_cols<S>(), s>>>(a, mode, hrows, hhat, npsf);
+    const int nchunk = (S / 2 + 1 + GC<S>::NB - 1) / GC<S>::NB;
+    k_cols<S><<<ntiles * nchunk, GC<S>::NTH, smem_cols<S>(), s>>>(a, mode, hrows, hhat, npsf);
     return cudaGetLastError();
 }
 template <int S>
 static cudaError_t run_rows_inv(const FftArgs &a, int ntiles, int T, int mode, cudaStream_t s) {
     if (ntiles == 0) return cudaSuccess;
-    const int nblk = (T + Geo<S>::ROWS - 1) / Geo<S>::ROWS;
-    k_rows_inv<S><<<ntiles * nblk, NT, smem_rows_inv<S>(T), s>>>(a, mode);
+    const int nblk = (T + GR<S>::NB - 1) / GR<S>::NB;
+    k_rows_inv<S><<<ntiles * nblk, GR<S>::NTH, smem_rows_inv<S>(T), s>>>(a, mode);
     return cudaGetLastError();
 }
 
@@ -569,6 +728,16 @@ static cudaError_t do_rows_inv(int S, const FftArgs &a, int nt, int T, int mode,
     FFT_DISPATCH(S, return run_rows_inv<SS>(a, nt, T, mode, s));
     return cudaSuccess;
 }
+template <int S>
+static cudaError_t geom(int &ldf, int &nb) {
+    ldf = LD<S>::LDF;
+    nb = GR<S>::NB;
+    return cudaSuccess;
+}
+static cudaError_t do_geom(int S, int &ldf, int &nb) {
+    FFT_DISPATCH(S, return geom<SS>(ldf, nb));
+    return cudaSuccess;
+}
 static cudaError_t do_attrs(int S, int T) {
     FFT_DISPATCH(S, return setup_attrs<SS>(T));
     return cudaSuccess;
@@ -593,7 +762,8 @@ FftPlan *fft_create(const Plan &pl, const std::vector<int> &local, const std::ve
     f->wy = d_wy; f->wx = d_wx; f->Ny = (int)pl.ny; f->Nx = (int)pl.nx;
     f->nlocal = (int)local.size();
     const int S = f->S, T = f->T, P = f->P;
-    const int LDF = S / 2 + 16;
+    int LDF = 0, rows_nb = 0;
+    if (do_geom(S, LDF, rows_nb) != cudaSuccess) return fail("bad FFT size");
     // active ranges
     auto range = [](const float *w, int G, int64_t n, int64_t a, int64_t b, int &lo, int &hi) {
         a = std::max<int64_t>(0, a); b = std::min<int64_t>(n, b);
@@ -648,7 +818,7 @@ FftPlan *fft_create(const Plan &pl, const std::vector<int> &local, const std::ve
     FC(dalloc((void **)&f->psf_slot, sizeof(int) * f->K));
     FC(dalloc((void **)&f->d_tH, sizeof(TileDesc) * std::max<size_t>(1, f->tH.size())));
     FC(dalloc((void **)&f->d_tHT, sizeof(TileDesc) * std::max<size_t>(1, f->tHT.size())));
-    f->nblk_inv = (T + (S >= 512 ? 8 : 16) - 1) / (S >= 512 ? 8 : 16);
+    f->nblk_inv = (T + rows_nb - 1) / rows_nb;
     FC(dalloc((void **)&f->partials, sizeof(double) * std::max<size_t>(1, f->tH.size() * f->nblk_inv)));
     f->h_part.resize(std::max<size_t>(1, f->tH.size() * f->nblk_inv));
     // twiddles in fp64, rounded (A24)
