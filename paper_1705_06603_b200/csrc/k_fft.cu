@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "epilogue.cuh"
@@ -642,16 +643,20 @@ struct FftPlan {
     }
 };
 
-// FFT size per P: minimise S^2 log2(S) / T^2 (work per valid pixel), T = S - P + 1
+// FFT size per P: minimise S^2 log2(S) / T^2 (work per valid pixel), T = S - P + 1,
+// over S <= 512; S = 1024 only when P leaves fewer than 64 valid rows at 512.
+// Measured at P = 63 (c4, B200): S = 256 / 512 / 1024 -> 9856 / 9880 / 5924 Mpix-it/s;
+// the 1024 kernels run 1 CTA per SM (smem) and are latency-bound.
 static int choose_S(int P) {
     int best = 0;
     double bc = 1e300;
-    for (int S = 64; S <= 1024; S *= 2) {
+    for (int S = 64; S <= 512; S *= 2) {
         const int T = S - P + 1;
         if (T < 8) continue;
-        const double c = (double)S * S * std::log2((double)S) / ((double)T * T) * (1.0 + 0.02 * std::log2((double)S));
+        const double c = (double)S * S * std::log2((double)S) / ((double)T * T);
         if (c < bc) { bc = c; best = S; }
     }
+    if (512 - P + 1 < 64 && 1024 - P + 1 >= 8) best = 1024;
     return best;
 }
 
@@ -755,6 +760,10 @@ FftPlan *fft_create(const Plan &pl, const std::vector<int> &local, const std::ve
     } while (0)
     f->P = pl.P;
     f->S = choose_S(pl.P);
+    if (const char *ov = std::getenv("DEBLUR_FFT_SIZE")) {      // measurement override (crossover sweeps)
+        const int v = std::atoi(ov);
+        if (v >= 64 && v <= 1024 && (v & (v - 1)) == 0 && v - pl.P + 1 >= 8) f->S = v;
+    }
     if (!f->S) return fail("no FFT size fits P");
     f->T = f->S - f->P + 1;
     f->Gx = Gx;
