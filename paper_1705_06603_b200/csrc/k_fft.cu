@@ -26,6 +26,8 @@
 #include <cstdlib>
 #include <vector>
 
+#include <cuda_pipeline.h>
+
 #include "epilogue.cuh"
 #include "fft.hpp"
 
@@ -256,20 +258,31 @@ __global__ void __launch_bounds__(256) k_rows_fwd(FftArgs A, int mode, int par, 
         if (mode == 0) { q0 = t.q0; nq = t.q1 - t.q0 + 1; }
     }
     for (int i = tid; i < S; i += G::NTH) Wsm[i] = A.W[i];
-    for (int idx = tid; idx < NB * S; idx += G::NTH) {
-        const int rr = idx / S, cc = idx - rr * S;
-        const int row = r0 + rr;
-        float v = 0.f;
+    {
+        // batched loads (all in flight before the first use): real rows of the window
+        constexpr int LPT = NB * S / G::NTH;
+        const float *src;
+        int64_t pitch;
+        int gy0, gx0, limy, limx;
         if (mode == 0) {
-            const int ly = t.y0 + row, lx = t.x0 + cc;
-            if (ly < Fd->ny && lx < Fd->nx) v = Fd->x[par][(int64_t)ly * Fd->ep + lx];
+            src = Fd->x[par]; pitch = Fd->ep; gy0 = t.y0 + r0; gx0 = t.x0; limy = Fd->ny; limx = Fd->nx;
         } else if (mode == 1) {
-            const int ri = t.y0 - c2 + row, rj = t.x0 - c2 + cc;
-            if (ri >= 0 && ri < Fd->my && rj >= 0 && rj < Fd->mx) v = Fd->r[(int64_t)ri * Fd->op + rj];
+            src = Fd->r; pitch = Fd->op; gy0 = t.y0 - c2 + r0; gx0 = t.x0 - c2; limy = Fd->my; limx = Fd->mx;
         } else {
-            if (row < P && cc < P) v = psfs[(int64_t)tile * P * P + row * P + cc];
+            src = psfs + (int64_t)tile * P * P; pitch = P; gy0 = r0; gx0 = 0; limy = P; limx = P;
         }
-        xs[rr * XS + cc] = v;
+        float vals[LPT];
+#pragma unroll
+        for (int it = 0; it < LPT; ++it) {
+            const int idx = tid + it * G::NTH, rr = idx / S, cc = idx % S;
+            const int gy = gy0 + rr, gx = gx0 + cc;
+            vals[it] = (gy >= 0 && gy < limy && gx >= 0 && gx < limx) ? __ldg(src + (int64_t)gy * pitch + gx) : 0.f;
+        }
+#pragma unroll
+        for (int it = 0; it < LPT; ++it) {
+            const int idx = tid + it * G::NTH, rr = idx / S, cc = idx % S;
+            xs[rr * XS + cc] = vals[it];
+        }
     }
     for (int qi = 0; qi < nq; ++qi) {
         if (mode == 0) {
@@ -322,25 +335,42 @@ __global__ void __launch_bounds__(256) k_rows_fwd(FftArgs A, int mode, int par, 
 }
 
 // ------------------------------------------------------------------ pass B / B'
+// Hhat chunk (S rows x NB columns starting at f0) -> smem hbuf[n][t] with cp.async
+template <int S, int NB, int NTH, int LDF>
+__device__ __forceinline__ void prefetch_hhat(float2 *hbuf, const float2 *Hk_f0, int tid) {
+    constexpr int V = NB / 2;                 // 16-byte vectors per row
+    constexpr int N = S * V;
+#pragma unroll
+    for (int it = 0; it < (N + NTH - 1) / NTH; ++it) {
+        const int idx = tid + it * NTH;
+        if (idx < N) {
+            const int n = idx / V, v = idx % V;
+            __pipeline_memcpy_async(hbuf + n * NB + 2 * v, Hk_f0 + (int64_t)n * LDF + 2 * v, 16);
+        }
+    }
+    __pipeline_commit();
+}
+
 // mode 0: H; 1: H^T; 2: PSF spectra (forward column DFT of hrows -> Hhat)
 template <int S>
 __global__ void __launch_bounds__(512) k_cols(FftArgs A, int mode, const float2 *hrows, float2 *hhat, int npsf) {
     using G = GC<S>;
     using F = typename G::F;
-    constexpr int NB = G::NB, CS = G::CS, E = G::E, LDF = LD<S>::LDF, NF = S / 2 + 1;
+    constexpr int NB = G::NB, CS = G::CS, E = G::E, LDF = LD<S>::LDF, NF = S / 2 + 1, NTH = G::NTH;
     using S0 = typename F::First;
     using SL = typename F::Last;
     static_assert(S0::R == SL::R, "first/last radix must match");
     extern __shared__ __align__(16) float2 sm2[];
     float2 *Wsm = sm2;               // S
-    float2 *colq = Wsm + S;          // NB x CS
+    float2 *hbuf = Wsm + S;          // S x NB (prefetched PSF spectrum chunk)
+    float2 *colq = hbuf + S * NB;    // NB x CS
     float2 *work = colq + NB * CS;   // NB x CS
     float *wys = reinterpret_cast<float *>(work + NB * CS);   // S
     const int tid = threadIdx.x;
     const int nchunk = (NF + NB - 1) / NB;
     const int tile = blockIdx.x / nchunk, f0 = (blockIdx.x % nchunk) * NB;
     const int P = A.P, c2 = P - 1, T = S - P + 1;
-    for (int i = tid; i < S; i += G::NTH) Wsm[i] = A.W[i];
+    for (int i = tid; i < S; i += NTH) Wsm[i] = A.W[i];
     __syncthreads();
     float2 v[E];
 
@@ -370,6 +400,11 @@ __global__ void __launch_bounds__(512) k_cols(FftArgs A, int mode, const float2 
     const TileDesc td = A.tiles[tile];
     const FacetDev &Fd = A.facets[td.f];
     float2 *base = A.scratch + (int64_t)tile * A.tile_rows * LDF;
+    auto hk = [&](int p, int q) { return A.Hhat + (int64_t)A.psf_slot[p * A.Gx + q] * S * LDF + f0; };
+    auto fill_wys = [&](int p) {
+        const float *wyp = A.wy + (size_t)p * A.Ny + Fd.ey0 + td.y0;
+        for (int i = tid; i < S; i += NTH) wys[i] = (td.y0 + i < Fd.ny) ? __ldg(wyp + i) : 0.f;
+    };
 
     if (mode == 0) {
         float2 acc[E];
@@ -377,15 +412,25 @@ __global__ void __launch_bounds__(512) k_cols(FftArgs A, int mode, const float2 
         for (int e = 0; e < E; ++e) acc[e] = make_float2(0.f, 0.f);
         for (int q = td.q0; q <= td.q1; ++q) {
             __syncthreads();
-            const float2 *Aq = base + (int64_t)(q - td.q0) * S * LDF + f0;
-            for (int idx = tid; idx < NB * S; idx += G::NTH) {
-                const int c = idx % NB, row = idx / NB;
-                colq[c * CS + row] = Aq[(int64_t)row * LDF + c];
+            {   // batched load of the row-spectrum chunk of A_q
+                constexpr int LPT = NB * S / NTH;
+                const float2 *Aq = base + (int64_t)(q - td.q0) * S * LDF + f0;
+                float2 tmp[LPT];
+#pragma unroll
+                for (int it = 0; it < LPT; ++it) {
+                    const int idx = tid + it * NTH;
+                    tmp[it] = __ldg(Aq + (int64_t)(idx / NB) * LDF + (idx % NB));
+                }
+#pragma unroll
+                for (int it = 0; it < LPT; ++it) {
+                    const int idx = tid + it * NTH;
+                    colq[(idx % NB) * CS + idx / NB] = tmp[it];
+                }
             }
             for (int p = td.p0; p <= td.p1; ++p) {
                 __syncthreads();
-                const float *wyp = A.wy + (size_t)p * A.Ny + Fd.ey0 + td.y0;
-                for (int i = tid; i < S; i += G::NTH) wys[i] = (td.y0 + i < Fd.ny) ? __ldg(wyp + i) : 0.f;
+                prefetch_hhat<S, NB, NTH, LDF>(hbuf, hk(p, q), tid);   // overlaps the FFT below
+                fill_wys(p);
                 __syncthreads();
                 // stage 0 from colq, weighted by the row weight wy_p (constant along the row)
 #pragma unroll
@@ -402,15 +447,15 @@ __global__ void __launch_bounds__(512) k_cols(FftArgs A, int mode, const float2 
                     S0::template bfly<-1>(&v[i * S0::R], j, Wsm, S);
                 }
                 F::template middle<-1>(work, v, tid, Wsm, S);
-                const int slot = A.psf_slot[p * A.Gx + q];
-                const float2 *Hk = A.Hhat + (int64_t)slot * S * LDF + f0;
+                __pipeline_wait_prior(0);
+                __syncthreads();
 #pragma unroll
                 for (int i = 0; i < SL::BPT; ++i) {
                     int t, j;
                     SL::bj(i, tid, t, j);
 #pragma unroll
                     for (int r = 0; r < SL::R; ++r) {
-                        const float2 h = __ldg(Hk + (int64_t)SL::out_n(j, r) * LDF + t);
+                        const float2 h = hbuf[SL::out_n(j, r) * NB + t];
                         acc[i * SL::R + r] = cadd(acc[i * SL::R + r], cmul(v[i * SL::R + r], h));
                     }
                 }
@@ -440,12 +485,13 @@ __global__ void __launch_bounds__(512) k_cols(FftArgs A, int mode, const float2 
     }
 
     // mode 1 (H^T): R-hat = DFT_y of the r-window spectrum rows, kept in colq
+    if (td.p0 <= td.p1 && td.q0 <= td.q1) prefetch_hhat<S, NB, NTH, LDF>(hbuf, hk(td.p0, td.q0), tid);
 #pragma unroll
     for (int i = 0; i < S0::BPT; ++i) {
         int t, j;
         S0::bj(i, tid, t, j);
 #pragma unroll
-        for (int r = 0; r < S0::R; ++r) v[i * S0::R + r] = base[(int64_t)S0::in_n(j, r) * LDF + f0 + t];
+        for (int r = 0; r < S0::R; ++r) v[i * S0::R + r] = __ldg(base + (int64_t)S0::in_n(j, r) * LDF + f0 + t);
         S0::template bfly<-1>(&v[i * S0::R], j, Wsm, S);
     }
     F::template middle<-1>(work, v, tid, Wsm, S);
@@ -457,11 +503,9 @@ __global__ void __launch_bounds__(512) k_cols(FftArgs A, int mode, const float2 
         for (int e = 0; e < E; ++e) acc[e] = make_float2(0.f, 0.f);
         for (int p = td.p0; p <= td.p1; ++p) {
             __syncthreads();
-            const float *wyp = A.wy + (size_t)p * A.Ny + Fd.ey0 + td.y0;
-            for (int i = tid; i < S; i += G::NTH) wys[i] = (td.y0 + i < Fd.ny) ? __ldg(wyp + i) : 0.f;
+            fill_wys(p);
+            __pipeline_wait_prior(0);
             __syncthreads();
-            const int slot = A.psf_slot[p * A.Gx + q];
-            const float2 *Hk = A.Hhat + (int64_t)slot * S * LDF + f0;
 #pragma unroll
             for (int i = 0; i < S0::BPT; ++i) {
                 int t, j;
@@ -469,9 +513,15 @@ __global__ void __launch_bounds__(512) k_cols(FftArgs A, int mode, const float2 
 #pragma unroll
                 for (int r = 0; r < S0::R; ++r) {
                     const int n = S0::in_n(j, r);
-                    v[i * S0::R + r] = cmulc(colq[t * CS + n], __ldg(Hk + (int64_t)n * LDF + t));
+                    v[i * S0::R + r] = cmulc(colq[t * CS + n], hbuf[n * NB + t]);
                 }
                 S0::template bfly<+1>(&v[i * S0::R], j, Wsm, S);
+            }
+            __syncthreads();      // hbuf consumed: prefetch the next PSF spectrum under the FFT
+            {
+                int np = p + 1, nq = q;
+                if (np > td.p1) { np = td.p0; ++nq; }
+                if (nq <= td.q1) prefetch_hhat<S, NB, NTH, LDF>(hbuf, hk(np, nq), tid);
             }
             F::template middle<+1>(work, v, tid, Wsm, S);
 #pragma unroll
@@ -511,18 +561,28 @@ __device__ __forceinline__ void c2r_rows(const float2 *__restrict__ src0, int nr
     using F = typename G::F;
     constexpr int NB = G::NB, SH = G::SH, RS = G::RS, XS = G::XS, LDF = LD<S>::LDF;
     const int tid = threadIdx.x;
-    for (int idx = tid; idx < NB * SH; idx += G::NTH) {
-        const int rr = idx / SH, k = idx - rr * SH;
-        float2 zz = make_float2(0.f, 0.f);
+    constexpr int LPT = NB * SH / G::NTH;
+    float2 xk[LPT], xc[LPT];
+#pragma unroll
+    for (int it = 0; it < LPT; ++it) {
+        const int idx = tid + it * G::NTH, rr = idx / SH, k = idx % SH;
         if (rr < nrows) {
             const float2 *X = src0 + (int64_t)rr * LDF;
-            const float2 xk = X[k], xc = conjf2(X[SH - k]);
-            const float2 e = make_float2(0.5f * (xk.x + xc.x), 0.5f * (xk.y + xc.y));
-            const float2 d = make_float2(0.5f * (xk.x - xc.x), 0.5f * (xk.y - xc.y));
-            const float2 o = cmul(d, conjf2(Wsm[k]));     // O_k
-            zz = make_float2(e.x - o.y, e.y + o.x);      // E + i O
+            xk[it] = __ldg(X + k);
+            xc[it] = __ldg(X + SH - k);
+        } else {
+            xk[it] = make_float2(0.f, 0.f);
+            xc[it] = make_float2(0.f, 0.f);
         }
-        work[rr * RS + k] = zz;
+    }
+#pragma unroll
+    for (int it = 0; it < LPT; ++it) {
+        const int idx = tid + it * G::NTH, rr = idx / SH, k = idx % SH;
+        const float2 b = conjf2(xc[it]);
+        const float2 e = make_float2(0.5f * (xk[it].x + b.x), 0.5f * (xk[it].y + b.y));
+        const float2 d = make_float2(0.5f * (xk[it].x - b.x), 0.5f * (xk[it].y - b.y));
+        const float2 o = cmul(d, conjf2(Wsm[k]));     // O_k
+        work[rr * RS + k] = make_float2(e.x - o.y, e.y + o.x);   // E + i O
     }
     __syncthreads();
     float2 v[G::E];
@@ -566,19 +626,35 @@ __global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
     if (mode != INV_HT) {
         c2r_rows<S>(base + ((int64_t)A.NQ * S + r0) * LDF, nrows, work, outs, Wsm);
         double dsum = 0.0;
-        for (int idx = tid; idx < nrows * T; idx += G::NTH) {
-            const int rr = idx / T, cc = idx - rr * T;
-            const int oi = t.y0 + r0 + rr, oj = t.x0 + cc;
-            if (oi >= Fd.my || oj >= Fd.mx) continue;
-            const float hx = outs[rr * XS + c2 + cc] * scale;
-            const int64_t o = (int64_t)oi * Fd.op + oj;
-            if (mode == FFT_PLAIN) {
-                Fd.r[o] = hx;
-            } else {
-                const float wv = Fd.w ? Fd.w[o] : Fd.w_scalar;
-                const float d = hx - Fd.y[o];
-                if (mode == FFT_RESIDUAL) Fd.r[o] = wv * d;
-                dsum += 0.5 * (double)wv * (double)d * (double)d;
+        constexpr int U = 8;
+        const int ntot = nrows * T;
+        for (int b0 = 0; b0 < ntot; b0 += U * G::NTH) {
+            float yv[U], wv[U];
+            int64_t off[U];
+            bool ok[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int idx = b0 + tid + u * G::NTH;
+                const int rr = idx / T, cc = idx - rr * T;
+                const int oi = t.y0 + r0 + rr, oj = t.x0 + cc;
+                ok[u] = idx < ntot && oi < Fd.my && oj < Fd.mx;
+                off[u] = (int64_t)oi * Fd.op + oj;
+                yv[u] = (ok[u] && mode != FFT_PLAIN) ? __ldg(Fd.y + off[u]) : 0.f;
+                wv[u] = (ok[u] && mode != FFT_PLAIN) ? (Fd.w ? __ldg(Fd.w + off[u]) : Fd.w_scalar) : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (!ok[u]) continue;
+                const int idx = b0 + tid + u * G::NTH;
+                const int rr = idx / T, cc = idx - rr * T;
+                const float hx = outs[rr * XS + c2 + cc] * scale;
+                if (mode == FFT_PLAIN) {
+                    Fd.r[off[u]] = hx;
+                } else {
+                    const float d = hx - yv[u];
+                    if (mode == FFT_RESIDUAL) Fd.r[off[u]] = wv[u] * d;
+                    dsum += 0.5 * (double)wv[u] * (double)d * (double)d;
+                }
             }
         }
         if (mode != FFT_PLAIN && A.partials) {
@@ -671,11 +747,11 @@ static size_t smem_rows_fwd() {
     return (size_t)S * 8 + (size_t)G::NB * G::RS * 8 + (size_t)G::NB * G::XS * 4 + (size_t)S * 4;
 }
 template <int S>
-static size_t smem_cols() { using G = GC<S>; return (size_t)S * 8 + 2 * (size_t)G::NB * G::CS * 8 + (size_t)S * 4; }
+static size_t smem_cols() { using G = GC<S>; return (size_t)S * 8 + (size_t)S * G::NB * 8 + 2 * (size_t)G::NB * G::CS * 8 + (size_t)S * 4; }
 template <int S>
-static size_t smem_rows_inv(int T) {
+static size_t smem_rows_inv(int T, bool ht = true) {
     using G = GR<S>;
-    return (size_t)S * 8 + (size_t)G::NB * G::RS * 8 + (size_t)G::NB * G::XS * 4 + (size_t)G::NB * T * 4;
+    return (size_t)S * 8 + (size_t)G::NB * G::RS * 8 + (size_t)G::NB * G::XS * 4 + (ht ? (size_t)G::NB * T * 4 : 0);
 }
 
 template <int S>
@@ -705,7 +781,7 @@ template <int S>
 static cudaError_t run_rows_inv(const FftArgs &a, int ntiles, int T, int mode, cudaStream_t s) {
     if (ntiles == 0) return cudaSuccess;
     const int nblk = (T + GR<S>::NB - 1) / GR<S>::NB;
-    k_rows_inv<S><<<ntiles * nblk, GR<S>::NTH, smem_rows_inv<S>(T), s>>>(a, mode);
+    k_rows_inv<S><<<ntiles * nblk, GR<S>::NTH, smem_rows_inv<S>(T, mode == INV_HT), s>>>(a, mode);
     return cudaGetLastError();
 }
 
