@@ -100,26 +100,6 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def algorithmic_fma(pb, boxes, which: str) -> float:
-    """a*P^2 FMA per output pixel, a = #{k : omega_k(pixel) != 0}.
-    H: output = observed pixel, omega at its centre (i+c, j+c); H^T: estimate pixel."""
-    c = (pb.P - 1) // 2
-    nzy = (pb.wy != 0).sum(axis=0).astype(np.float64)    # active grid rows per estimate row
-    nzx = (pb.wx != 0).sum(axis=0).astype(np.float64)
-    cy, cx = np.concatenate([[0], np.cumsum(nzy)]), np.concatenate([[0], np.cumsum(nzx)])
-    tot = 0.0
-    for b in boxes:
-        oy0, oy1, ox0, ox1, ey0, ey1, ex0, ex1 = [int(v) for v in b]
-        if which == "H":
-            ry = cy[oy1 + c] - cy[oy0 + c]
-            rx = cx[ox1 + c] - cx[ox0 + c]
-        else:
-            ry = cy[ey1] - cy[ey0]
-            rx = cx[ex1] - cx[ex0]
-        tot += ry * rx
-    return tot * pb.P * pb.P
-
-
 def run_ours(args, rank, world, local):
     import torch
     from paper_1705_06603_b200 import deblur as D
@@ -140,7 +120,6 @@ def run_ours(args, rank, world, local):
     path = {"direct": D.CONV_DIRECT, "fft": D.CONV_FFT, "auto": D.CONV_AUTO}[args.path]
     params, keep = D.problem_params(pb, conv_path=path, rank=rank, world=world, device=local, nccl_id_bytes=nid)
     dev = D.Deblur(params, keep)
-    boxes, owner = D.plan_facets(params)
     stream = torch.cuda.ExternalStream(dev.stream)
 
     def barrier():
@@ -170,28 +149,38 @@ def run_ours(args, rank, world, local):
     npix = pb.ny * pb.nx
     value = npix * args.steps / (ms / 1e3) / 1e6
 
-    # dominant kernel roofline (this rank's launches; per-launch averages)
+    # dominant kernel roofline (this rank's launches; per-launch averages; algorithmic work from the library)
     kern = {k: v for k, v in stats.items() if v[0] > 0 and k != "halo_exchange"}
     launches = sum(v[0] for v in kern.values())
-    dom = max(kern, key=lambda k: kern[k][1])
-    n_dom, ms_dom = kern[dom]
+    work = dev.kernel_work()
     pk = peaks()
-    my_boxes = [b for b, o in zip(boxes, owner) if o == rank]
-    roofline = None
-    if dom in ("H_direct_residual", "HT_direct_update"):
-        fma = algorithmic_fma(pb, my_boxes, "H" if dom.startswith("H_") else "HT")
-        achieved = 2 * fma / (ms_dom / n_dom / 1e3) / 1e12
-        peak = NOMINAL_SMS * FMA_PER_SM_CLK * 2 * pk.get("sm_max_mhz", 1965.0) / 1e6
-        roofline = {"bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
-                    "frac": round(achieved / peak, 4), "traffic": None,
-                    "kernel": dom, "ms_per_launch": round(ms_dom / n_dom, 4),
+    fp32_peak = NOMINAL_SMS * FMA_PER_SM_CLK * 2 * pk.get("sm_max_mhz", 1965.0) / 1e6   # TFLOP/s
+
+    def roof(name):
+        n, tot_ms = kern[name]
+        per = tot_ms / n / 1e3
+        fl, by = work.get(name, (0.0, 0.0))
+        if fl > 0:
+            a = fl / per / 1e12
+            return {"bound": "alu", "achieved": round(a, 3), "peak": round(fp32_peak, 2), "unit": "TFLOP/s",
+                    "frac": round(a / fp32_peak, 4), "traffic": None, "kernel": name,
+                    "ms_per_launch": round(per * 1e3, 4),
                     "peak_source": "148 SM x 128 FP32 FMA/clk x 2 x sm_max_mhz (guide unit counts)"}
-    else:
-        # HBM-bound kernels: algorithmic bytes per launch
-        roofline = {"bound": "hbm", "achieved": None, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": None,
-                    "traffic": None, "kernel": dom, "ms_per_launch": round(ms_dom / n_dom, 4)}
-    breakdown = {k: {"launches": v[0], "ms_per_launch": round(v[1] / max(v[0], 1), 4),
-                     "share": round(v[1] / max(sum(x[1] for x in kern.values()), 1e-9), 4)} for k, v in kern.items()}
+        a = by / per / 1e9 if by > 0 else None
+        return {"bound": "hbm", "achieved": None if a is None else round(a, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": None if a is None else round(a / pk["hbm_gbs"], 4), "traffic": None, "kernel": name,
+                "ms_per_launch": round(per * 1e3, 4),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "_fallback" not in pk else "fallback"}
+
+    dom = max(kern, key=lambda k: kern[k][1])
+    roofline = roof(dom)
+    tot_ms_all = sum(x[1] for x in kern.values())
+    breakdown = {}
+    for k, v in kern.items():
+        r = roof(k)
+        breakdown[k] = {"launches": v[0], "ms_per_launch": round(v[1] / max(v[0], 1), 4),
+                        "share": round(v[1] / max(tot_ms_all, 1e-9), 4),
+                        "achieved": r["achieved"], "unit": r["unit"], "frac": r["frac"]}
 
     # end to end through the C ABI with host buffers: reset(y from pinned host) + K iterations + image D2H
     y_pin = torch.from_numpy(pb.y).pin_memory()

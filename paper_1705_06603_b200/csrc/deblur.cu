@@ -32,11 +32,12 @@ thread_local std::string g_last_error;
 
 enum KClass {
     KC_H = 0, KC_HT_UPDATE, KC_CONSENSUS, KC_H_OBJ, KC_TV, KC_MAXDIFF, KC_XCHG, KC_HT_PLAIN, KC_H_PLAIN,
-    KC_FFT_H, KC_FFT_HT, KC_UPDATE_G, KC_COUNT
+    KC_FFT_H0, KC_FFT_H1, KC_FFT_H2, KC_FFT_HT0, KC_FFT_HT1, KC_FFT_HT2, KC_UPDATE_G, KC_COUNT
 };
 const char *k_names[KC_COUNT] = {"H_direct_residual", "HT_direct_update", "consensus", "H_direct_objective",
                                  "tv_value", "maxdiff", "halo_exchange", "HT_direct_plain", "H_direct_plain",
-                                 "H_fft_residual", "HT_fft", "update_from_g"};
+                                 "H_fft_rows", "H_fft_cols", "H_fft_rows_inv", "HT_fft_rows", "HT_fft_cols",
+                                 "HT_fft_rows_inv", "update_from_g"};
 
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
@@ -343,19 +344,36 @@ static deblur_status finish(deblur_t h) {
     return DEBLUR_OK;
 }
 
+static deblur_status run_fft_H(deblur_t h, const FacetDev *facets, int par, int mode) {
+    for (int pass = 0; pass < 3; ++pass) {
+        cudaEvent_t ev = nullptr;
+        h->prof_begin(KC_FFT_H0 + pass, &ev);
+        CU(fft_H_pass(*h->fft, pass, facets, par, mode, h->stream));
+        h->prof_end(KC_FFT_H0 + pass, ev);
+    }
+    return DEBLUR_OK;
+}
+
+static deblur_status run_fft_HT(deblur_t h, const FacetDev *facets) {
+    for (int pass = 0; pass < 3; ++pass) {
+        cudaEvent_t ev = nullptr;
+        h->prof_begin(KC_FFT_HT0 + pass, &ev);
+        CU(fft_HT_pass(*h->fft, pass, facets, h->stream));
+        h->prof_end(KC_FFT_HT0 + pass, ev);
+    }
+    return DEBLUR_OK;
+}
+
 // One Local-Solver step on every local facet (K1 + K2, or the FFT path + K4).
 static deblur_status local_step(deblur_t h, int last) {
     cudaEvent_t ev = nullptr;
     if (h->conv_path == DEBLUR_CONV_FFT) {
-        h->prof_begin(KC_FFT_H, &ev);
-        CU(fft_H(*h->fft, h->d_facets, h->par, FFT_RESIDUAL, h->stream));
-        h->prof_end(KC_FFT_H, ev);
-        h->prof_begin(KC_FFT_HT, &ev);
-        CU(fft_HT(*h->fft, h->d_facets, h->stream));
-        h->prof_end(KC_FFT_HT, ev);
+        deblur_status st;
+        if ((st = run_fft_H(h, h->d_facets, h->par, FFT_RESIDUAL)) != DEBLUR_OK) return st;
+        if ((st = run_fft_HT(h, h->d_facets)) != DEBLUR_OK) return st;
         h->prof_begin(KC_UPDATE_G, &ev);
         CU(launch_update_from_g(h->d_facets, h->d_tilesHT, (int)h->tilesHT.size(), h->plan.P, h->par, last, h->sc,
-                                h->d_partials, h->stream));
+                                nullptr, h->stream));
         h->prof_end(KC_UPDATE_G, ev);
     } else {
         h->prof_begin(KC_H, &ev);
@@ -693,9 +711,7 @@ deblur_status deblur_objective(deblur_t h, double out[4]) {
     cudaEvent_t ev = nullptr;
     // data term at the current x (A22)
     if (h->conv_path == DEBLUR_CONV_FFT) {
-        h->prof_begin(KC_FFT_H, &ev);
-        CU(fft_H(*h->fft, h->d_facets, h->par, FFT_OBJECTIVE, h->stream));
-        h->prof_end(KC_FFT_H, ev);
+        if ((s = run_fft_H(h, h->d_facets, h->par, FFT_OBJECTIVE)) != DEBLUR_OK) return s;
         CU(cudaStreamSynchronize(h->stream));
         std::vector<double> fd;
         CU(fft_data_partials(*h->fft, fd));
@@ -823,13 +839,11 @@ static deblur_status apply_common(deblur_t h, bool adjoint, const float *in, boo
     cudaEvent_t ev = nullptr;
     if (h->conv_path == DEBLUR_CONV_FFT) {
         if (!adjoint) {
-            h->prof_begin(KC_FFT_H, &ev);
-            CU(fft_H(*h->fft, h->d_facets_alt, 0, FFT_PLAIN, h->stream));
-            h->prof_end(KC_FFT_H, ev);
+            deblur_status st = run_fft_H(h, h->d_facets_alt, 0, FFT_PLAIN);
+            if (st != DEBLUR_OK) return st;
         } else {
-            h->prof_begin(KC_FFT_HT, &ev);
-            CU(fft_HT(*h->fft, h->d_facets, h->stream));
-            h->prof_end(KC_FFT_HT, ev);
+            deblur_status st = run_fft_HT(h, h->d_facets);
+            if (st != DEBLUR_OK) return st;
         }
     } else if (!adjoint) {
         h->prof_begin(KC_H_PLAIN, &ev);
@@ -1043,6 +1057,57 @@ deblur_status deblur_kernel_stats(deblur_t h, int32_t *n_classes, int64_t *launc
         if (ms) ms[i] = h->stat_ms[i];
     }
     *n_classes = KC_COUNT;
+    return DEBLUR_OK;
+}
+
+deblur_status deblur_kernel_work(deblur_t h, int32_t cls, double *flops, double *bytes) {
+    if (!h || !flops || !bytes || cls < 0 || cls >= KC_COUNT) return DEBLUR_EINVAL;
+    *flops = 0.0;
+    *bytes = 0.0;
+    const Plan &pl = h->plan;
+    const double P2 = (double)pl.P * pl.P;
+    // a(pixel) = #{k : omega_k(pixel) != 0} = nzy(row) * nzx(col) (separable hats)
+    auto nz_sum = [&](const std::vector<float> &w, int G, int64_t n, int64_t a, int64_t b) {
+        double t = 0;
+        for (int64_t i = a; i < b; ++i) {
+            int c = 0;
+            for (int g = 0; g < G; ++g) c += w[(size_t)g * n + i] != 0.f;
+            t += c;
+        }
+        return t;
+    };
+    const int c = (pl.P - 1) / 2;
+    double est_px = 0, obs_px = 0;
+    for (int id : h->local) {
+        const FacetPlan &f = pl.facets[id];
+        est_px += (double)(f.ey1 - f.ey0) * (f.ex1 - f.ex0);
+        obs_px += (double)(f.oy1 - f.oy0) * (f.ox1 - f.ox0);
+        if (cls == KC_H || cls == KC_H_OBJ || cls == KC_H_PLAIN)
+            *flops += 2.0 * P2 * nz_sum(h->h_wy, h->prm.psf_gy, pl.ny, f.oy0 + c, f.oy1 + c) *
+                      nz_sum(h->h_wx, h->prm.psf_gx, pl.nx, f.ox0 + c, f.ox1 + c);
+        if (cls == KC_HT_UPDATE || cls == KC_HT_PLAIN)
+            *flops += 2.0 * P2 * nz_sum(h->h_wy, h->prm.psf_gy, pl.ny, f.ey0, f.ey1) *
+                      nz_sum(h->h_wx, h->prm.psf_gx, pl.nx, f.ex0, f.ex1);
+    }
+    if (cls >= KC_FFT_H0 && cls <= KC_FFT_HT2 && h->fft)
+        *bytes = fft_pass_bytes(*h->fft, cls >= KC_FFT_HT0, (cls - KC_FFT_H0) % 3);
+    if (cls == KC_UPDATE_G) *bytes = 20.0 * est_px;            // g, u, x in; x+, u|v out
+    if (cls == KC_HT_UPDATE) *bytes = 24.0 * est_px;           // r (~obs), x, u in; x+, u|v out
+    if (cls == KC_H) *bytes = 4.0 * est_px + 12.0 * obs_px;    // x, y, W in; r out
+    if (cls == KC_CONSENSUS) {
+        double b = 0;
+        for (const BandRect &r : h->rects) {
+            const FacetDev &F = h->fh[r.f];
+            for (int yy = r.y0; yy < r.y1; ++yy) {
+                const int cy = 1 + (yy < F.ay.b_prev || yy >= F.ay.b_next);
+                for (int xx = r.x0; xx < r.x1; ++xx) {
+                    const int cx = 1 + (xx < F.ax.b_prev || xx >= F.ax.b_next);
+                    b += 4.0 * cy * cx + 12.0;                     // v of each contributor; x+ in, u in/out
+                }
+            }
+        }
+        *bytes = b;
+    }
     return DEBLUR_OK;
 }
 

@@ -72,6 +72,51 @@ __device__ __forceinline__ float update_pixel(const FacetDev &F, const float *xh
     return phi;
 }
 
+// Same arithmetic as update_pixel, returning x+ and the dual/band values instead of
+// storing them (the caller vectorises the stores).  phi is computed only when asked.
+__device__ __forceinline__ float update_value(const FacetDev &F, const float *xh, int XH, int i, int j, int fy, int fx,
+                                              float g, float uc, const SolverConst &sc, bool want_phi, float &phi,
+                                              int last, bool &shared, float &u_new, float &v_new) {
+    const int ny = F.ny, nx = F.nx;
+    const bool neu = sc.tv_boundary == 1;
+    const float e2 = sc.eps * sc.eps;
+    auto X = [&](int a, int b) { return xh[a * XH + b]; };
+    const int fyu = (fy == 0) ? ny - 1 : fy - 1;
+    const int fxl = (fx == 0) ? nx - 1 : fx - 1;
+    const float xc = X(i, j);
+    const float dyc = (neu && fy == ny - 1) ? 0.f : X(i + 1, j) - xc;
+    const float dxc = (neu && fx == nx - 1) ? 0.f : X(i, j + 1) - xc;
+    const float dyu = (neu && fyu == ny - 1) ? 0.f : xc - X(i - 1, j);
+    const float dxu = (neu && fx == nx - 1) ? 0.f : X(i - 1, j + 1) - X(i - 1, j);
+    const float dyl = (neu && fy == ny - 1) ? 0.f : X(i + 1, j - 1) - X(i, j - 1);
+    const float dxl = (neu && fxl == nx - 1) ? 0.f : xc - X(i, j - 1);
+    float sc_c, sc_u, sc_l;
+    const float t2c = dyc * dyc + dxc * dxc;
+    phi = 0.f;
+    if (sc.reg_kind == 0) {
+        sc_c = rsqrtf(t2c + e2);
+        sc_u = rsqrtf(dyu * dyu + dxu * dxu + e2);
+        sc_l = rsqrtf(dyl * dyl + dxl * dxl + e2);
+        if (want_phi) phi = t2c / (sqrtf(t2c + e2) + sc.eps);
+    } else {
+        const float d = sc.eps;
+        const float tc = sqrtf(t2c), tu = sqrtf(dyu * dyu + dxu * dxu), tl = sqrtf(dyl * dyl + dxl * dxl);
+        sc_c = (tc <= d) ? 1.f : d / tc;
+        sc_u = (tu <= d) ? 1.f : d / tu;
+        sc_l = (tl <= d) ? 1.f : d / tl;
+        if (want_phi) phi = (tc <= d) ? 0.5f * t2c : d * (tc - 0.5f * d);
+    }
+    const float tdiv = dyu * sc_u - dyc * sc_c + dxl * sc_l - dxc * sc_c;
+    const float om = omega_axis(F.ay, fy) * omega_axis(F.ax, fx);
+    const float gt = g + sc.lambda * tdiv + sc.gamma * om * (xc - uc);
+    const float xn = fmaxf(0.f, xc - sc.tau * gt);
+    shared = fy < F.ay.b_prev || fy >= F.ay.b_next || fx < F.ax.b_prev || fx >= F.ax.b_next;
+    u_new = uc + sc.rho * (xn - uc);
+    v_new = 2.f * xn - uc;
+    (void)last;
+    return xn;
+}
+
 // stage the (TYh+2) x (TXh+2) circular halo of x[par] for a tile at (y0, x0)
 __device__ __forceinline__ void stage_halo(const FacetDev &F, float *xh, int XH, int YH, int y0, int x0, int par) {
     const float *__restrict__ x = F.x[par];

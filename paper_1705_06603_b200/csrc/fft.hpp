@@ -25,6 +25,15 @@ void fft_destroy(FftPlan *f);
 cudaError_t fft_H(FftPlan &f, const FacetDev *d_facets, int par, int mode, cudaStream_t s);
 // g = H^T r on every local facet (into FacetDev::g).
 cudaError_t fft_HT(FftPlan &f, const FacetDev *d_facets, cudaStream_t s);
+// single passes (0 rows forward, 1 columns, 2 rows inverse) for per-pass timing
+cudaError_t fft_H_pass(FftPlan &f, int pass, const FacetDev *d_facets, int par, int mode, cudaStream_t s);
+cudaError_t fft_HT_pass(FftPlan &f, int pass, const FacetDev *d_facets, cudaStream_t s);
+// algorithmic HBM bytes moved by one launch of a pass: the pass's
+// compulsory reads/writes of x / r / y / W and of the inter-pass spectra; the PSF
+// spectra (sized to stay L2-resident) are not counted.
+double fft_pass_bytes(const FftPlan &f, bool ht, int pass);
+int fft_size(const FftPlan &f);
+
 // per-local-facet data partial sums of the last fft_H call (after a stream sync).
 cudaError_t fft_data_partials(FftPlan &f, std::vector<double> &out);
 

@@ -958,6 +958,44 @@ cudaError_t fft_HT(FftPlan &f, const FacetDev *d_facets, cudaStream_t s) {
     return do_rows_inv(f.S, a, n, f.T, INV_HT, s);
 }
 
+cudaError_t fft_H_pass(FftPlan &f, int pass, const FacetDev *d_facets, int par, int mode, cudaStream_t s) {
+    FftArgs a = f.args(d_facets, false);
+    const int n = (int)f.tH.size();
+    if (pass == 0) return do_rows_fwd(f.S, a, n, 0, par, nullptr, 0, nullptr, s);
+    if (pass == 1) return do_cols(f.S, a, n, 0, nullptr, nullptr, 0, s);
+    return do_rows_inv(f.S, a, n, f.T, mode, s);
+}
+
+cudaError_t fft_HT_pass(FftPlan &f, int pass, const FacetDev *d_facets, cudaStream_t s) {
+    FftArgs a = f.args(d_facets, true);
+    const int n = (int)f.tHT.size();
+    if (pass == 0) return do_rows_fwd(f.S, a, n, 1, 0, nullptr, 0, nullptr, s);
+    if (pass == 1) return do_cols(f.S, a, n, 1, nullptr, nullptr, 0, s);
+    return do_rows_inv(f.S, a, n, f.T, INV_HT, s);
+}
+
+double fft_pass_bytes(const FftPlan &f, bool ht, int pass) {
+    const double S = f.S, T = f.T, NF = f.S / 2 + 1;
+    const double spec = S * NF * 8.0;       // one S x (S/2+1) complex spectrum
+    const double ospec = T * NF * 8.0;      // T valid rows of it
+    double b = 0.0;
+    for (const TileDesc &t : (ht ? f.tHT : f.tH)) {
+        const double nq = std::max(0, t.q1 - t.q0 + 1);
+        if (!ht) {
+            if (pass == 0) b += S * S * 4.0 + nq * spec;          // x window in, A_q out
+            else if (pass == 1) b += nq * spec + ospec;            // A_q in, O out
+            else b += ospec + T * T * 12.0;                        // O in; y, W in; r out
+        } else {
+            if (pass == 0) b += S * S * 4.0 + spec;               // r window in, R out
+            else if (pass == 1) b += spec + nq * ospec;            // R in, B_q out
+            else b += nq * ospec + T * T * 4.0;                    // B_q in, g out
+        }
+    }
+    return b;
+}
+
+int fft_size(const FftPlan &f) { return f.S; }
+
 cudaError_t fft_data_partials(FftPlan &f, std::vector<double> &out) {
     out.assign(f.nlocal, 0.0);
     const size_t n = f.tH.size() * f.nblk_inv;

@@ -18,26 +18,104 @@ namespace {
 
 constexpr int UT_TY = 32, UT_TX = 128;   // update tile (matches the H^T tile grid)
 
+// K4: tile of UT_TY x UT_TX pixels; each thread owns a 4-pixel strip in 4 rows.
+// x halo staged with 16-byte loads (interior tiles) or a wrapped scalar path
+// (tiles touching the facet border: circular D within the facet, A2).
 __global__ void __launch_bounds__(EPI_NT) k_update_from_g(const FacetDev *facets, const TileDesc *tiles, int par,
                                                            int last, SolverConst sc, double *partials) {
-    __shared__ float xh[(UT_TY + 2) * (UT_TX + 2)];
+    constexpr int XH = UT_TX + 8;                    // smem col c <-> facet col x0 - 4 + c
+    __shared__ __align__(16) float xh[(UT_TY + 2) * XH];
     __shared__ double red[EPI_NT / 32];
     const TileDesc t = tiles[blockIdx.x];
     const FacetDev &F = facets[t.f];
-    constexpr int XH = UT_TX + 2;
-    stage_halo(F, xh, XH, UT_TY + 2, t.y0, t.x0, par);
+    const float *__restrict__ x = F.x[par];
+    const int tid = threadIdx.x;
+    const bool interior = t.y0 >= 1 && t.y0 + UT_TY + 1 <= F.ny && t.x0 >= 4 && t.x0 + UT_TX + 4 <= F.nx;
+    if (interior) {
+        constexpr int NV = XH / 4;                   // float4 per smem row
+        for (int idx = tid; idx < (UT_TY + 2) * NV; idx += EPI_NT) {
+            const int i = idx / NV, v = idx - i * NV;
+            const float4 val = __ldg(reinterpret_cast<const float4 *>(x + (int64_t)(t.y0 - 1 + i) * F.ep + t.x0 - 4) + v);
+            *reinterpret_cast<float4 *>(xh + i * XH + 4 * v) = val;
+        }
+    } else {
+        for (int idx = tid; idx < (UT_TY + 2) * XH; idx += EPI_NT) {
+            const int i = idx / XH, c = idx - i * XH;
+            int fy = t.y0 - 1 + i, fx = t.x0 - 4 + c;
+            fy = ((fy % F.ny) + F.ny) % F.ny;
+            fx = ((fx % F.nx) + F.nx) % F.nx;
+            xh[idx] = x[(int64_t)fy * F.ep + fx];
+        }
+    }
     __syncthreads();
+    const int tx = tid & 31, ty = tid >> 5;          // 32 strips of 4 columns x 8 row groups
+    constexpr int KR = UT_TY / 8;
+    const int lx0 = 4 * tx, fx0 = t.x0 + lx0;
+    const bool full = fx0 + 3 < F.nx;
+    const float *__restrict__ gp = F.g;
+    float *__restrict__ up = F.u;
+    float *__restrict__ vp = F.v;
+    float *__restrict__ xo = F.x[par ^ 1];
+    // phase 1: every load of the strip in flight before any use
+    float gv[KR][4], uv[KR][4];
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+        const int fy = t.y0 + ty + 8 * k;
+        const int64_t o = (int64_t)fy * F.ep + fx0;
+        if (fy < F.ny && full) {
+            const float4 g4 = __ldg(reinterpret_cast<const float4 *>(gp + o));
+            const float4 u4 = *reinterpret_cast<const float4 *>(up + o);
+            gv[k][0] = g4.x; gv[k][1] = g4.y; gv[k][2] = g4.z; gv[k][3] = g4.w;
+            uv[k][0] = u4.x; uv[k][1] = u4.y; uv[k][2] = u4.z; uv[k][3] = u4.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const bool ok = fy < F.ny && fx0 + j < F.nx;
+                gv[k][j] = ok ? gp[o + j] : 0.f;
+                uv[k][j] = ok ? up[o + j] : 0.f;
+            }
+        }
+    }
     double rsum = 0.0;
-    for (int idx = threadIdx.x; idx < UT_TY * UT_TX; idx += EPI_NT) {
-        const int ly = idx / UT_TX, lx = idx - ly * UT_TX;
-        const int fy = t.y0 + ly, fx = t.x0 + lx;
-        if (fy >= F.ny || fx >= F.nx) continue;
-        const float g = F.g[(int64_t)fy * F.ep + fx];
-        rsum += (double)update_pixel(F, xh, XH, ly + 1, lx + 1, fy, fx, g, par, last, sc);
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+        const int ly = ty + 8 * k;
+        const int fy = t.y0 + ly;
+        if (fy >= F.ny || fx0 >= F.nx) continue;
+        const int64_t o = (int64_t)fy * F.ep + fx0;
+        float xn[4], nu[4], nv[4];
+        bool sh[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int fx = fx0 + j;
+            float phi;
+            xn[j] = update_value(F, xh, XH, ly + 1, lx0 + j + 4, fy, fx, gv[k][j], uv[k][j], sc, partials != nullptr,
+                                 phi, last, sh[j], nu[j], nv[j]);
+            if (fx < F.nx) rsum += (double)phi;
+        }
+        if (full) {
+            *reinterpret_cast<float4 *>(xo + o) = make_float4(xn[0], xn[1], xn[2], xn[3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (fx0 + j < F.nx) xo[o + j] = xn[j];
+        }
+        if (last) {
+            if (full && !sh[0] && !sh[1] && !sh[2] && !sh[3]) {
+                *reinterpret_cast<float4 *>(up + o) = make_float4(nu[0], nu[1], nu[2], nu[3]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (fx0 + j >= F.nx) continue;
+                    if (sh[j]) vp[o + j] = nv[j];
+                    else up[o + j] = nu[j];
+                }
+            }
+        }
     }
     if (partials) {
-        const double s = block_sum(rsum, red);
-        if (threadIdx.x == 0) partials[blockIdx.x] = s;
+        const double s2 = block_sum(rsum, red);
+        if (tid == 0) partials[blockIdx.x] = s2;
     }
 }
 

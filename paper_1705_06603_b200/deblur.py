@@ -83,6 +83,7 @@ def lib():
             "deblur_kernel_stats": ([h, _ip, _lp, _dp], ctypes.c_int),
             "deblur_kernel_name": ([ctypes.c_int32], ctypes.c_char_p),
             "deblur_reset_stats": ([h], ctypes.c_int),
+            "deblur_kernel_work": ([h, ctypes.c_int32, _dp, _dp], ctypes.c_int),
             "deblur_get_conv_path": ([h, _ip], ctypes.c_int),
             "deblur_get_stream": ([h, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
             "deblur_plan_facets": ([ctypes.POINTER(Params), _ip, _lp, _ip], ctypes.c_int),
@@ -101,7 +102,7 @@ EXPORTED = ["deblur_nccl_id", "deblur_create", "deblur_destroy", "deblur_apply_H
             "deblur_apply_H_device", "deblur_apply_HT_device", "deblur_iterate", "deblur_objective",
             "deblur_get_image", "deblur_state_size", "deblur_get_state", "deblur_set_state", "deblur_reset",
             "deblur_get_step", "deblur_set_profiling", "deblur_kernel_stats", "deblur_kernel_name",
-            "deblur_reset_stats", "deblur_get_conv_path", "deblur_get_stream", "deblur_plan_facets", "deblur_plan_messages",
+            "deblur_reset_stats", "deblur_kernel_work", "deblur_get_conv_path", "deblur_get_stream", "deblur_plan_facets", "deblur_plan_messages",
             "deblur_last_error"]
 
 
@@ -313,3 +314,17 @@ class Deblur:
         ms = (ctypes.c_double * 64)()
         self._c(self._lib.deblur_kernel_stats(self._h, ctypes.byref(n), launches, ms))
         return {self._lib.deblur_kernel_name(i).decode(): (int(launches[i]), float(ms[i])) for i in range(n.value)}
+
+    def kernel_work(self):
+        """{class name: (algorithmic flops, algorithmic bytes) per launch}."""
+        out = {}
+        i = 0
+        while True:
+            name = self._lib.deblur_kernel_name(i).decode()
+            if not name:
+                break
+            f, b = ctypes.c_double(0), ctypes.c_double(0)
+            self._c(self._lib.deblur_kernel_work(self._h, i, ctypes.byref(f), ctypes.byref(b)))
+            out[name] = (f.value, b.value)
+            i += 1
+        return out

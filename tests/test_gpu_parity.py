@@ -223,3 +223,20 @@ def test_zero_data_stays_zero():
         dev.iterate(3)
         x, u = dev.get_state()
     assert np.abs(x).max() == 0 and np.abs(u).max() == 0
+
+
+def test_kernel_work_counts():
+    """deblur_kernel_work's direct-path flop count equals an independent count of
+    2 a P^2 per output pixel (a = PSFs with nonzero weight at the pixel)."""
+    pb = synth.make_config(2, n=600, facets=(2, 2), overlap=64)
+    from oracle import geometry
+    fac = geometry.plan(pb.ny, pb.nx, pb.P, 2, 2, 64)
+    c = (pb.P - 1) // 2
+    ay = (pb.wy != 0).sum(0)
+    ax = (pb.wx != 0).sum(0)
+    fl_h = sum(2.0 * pb.P ** 2 * ay[f.oy[0] + c:f.oy[1] + c].sum() * ax[f.ox[0] + c:f.ox[1] + c].sum() for f in fac)
+    fl_ht = sum(2.0 * pb.P ** 2 * ay[f.ey[0]:f.ey[1]].sum() * ax[f.ex[0]:f.ex[1]].sum() for f in fac)
+    with D.Deblur.from_problem(pb, conv_path=D.CONV_DIRECT) as dev:
+        w = dev.kernel_work()
+    assert w["H_direct_residual"][0] == pytest.approx(fl_h, rel=1e-12)
+    assert w["HT_direct_update"][0] == pytest.approx(fl_ht, rel=1e-12)
