@@ -219,8 +219,9 @@ struct GR {
 // geometry of the column pass (length S complex transforms, NBC columns per CTA)
 template <int S>
 struct GC {
-    static constexpr int NTH = 512;
-    static constexpr int NB = (S <= 64) ? 64 : (S <= 128) ? 32 : (S <= 512) ? 16 : 8;
+    // 256 threads, 8 columns per CTA from S = 256 up: ~104 KB smem at S = 512, two CTAs per SM
+    static constexpr int NTH = (S <= 128) ? 512 : 256;
+    static constexpr int NB = (S <= 64) ? 64 : (S <= 128) ? 32 : 8;
     static constexpr int CS = S + ((NB >= 16) ? 1 : 16 / NB);
     using F = Fft<S, NB, CS, NTH>;
     static constexpr int E = F::E;
@@ -353,7 +354,7 @@ __device__ __forceinline__ void prefetch_hhat(float2 *hbuf, const float2 *Hk_f0,
 
 // mode 0: H; 1: H^T; 2: PSF spectra (forward column DFT of hrows -> Hhat)
 template <int S>
-__global__ void __launch_bounds__(512) k_cols(FftArgs A, int mode, const float2 *hrows, float2 *hhat, int npsf) {
+__global__ void __launch_bounds__(GC<S>::NTH) k_cols(FftArgs A, int mode, const float2 *hrows, float2 *hhat, int npsf) {
     using G = GC<S>;
     using F = typename G::F;
     constexpr int NB = G::NB, CS = G::CS, E = G::E, LDF = LD<S>::LDF, NF = S / 2 + 1, NTH = G::NTH;
