@@ -738,8 +738,9 @@ static int choose_S(int P) {
 }
 
 bool fft_prefer(int P) {
-    // Crossover: measured on B200; direct below, FFT at and above.
-    return P >= 31;
+    // Measured crossover (profiles/r1/crossover.jsonl; 4096^2, 8x8 PSFs, 1 facet, B200):
+    // direct 1.24 ms vs FFT 1.17 ms per step already at P = 7, FFT 5-80x faster from P = 15.
+    return P >= 7;
 }
 
 template <int S>
