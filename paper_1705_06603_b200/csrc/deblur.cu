@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -84,6 +85,10 @@ struct deblur_ctx {
     std::vector<cudaEvent_t> ev_pool;
     int64_t stat_n[KC_COUNT] = {0};
     double stat_ms[KC_COUNT] = {0};
+    // CUDA graphs of two full iterations (parity returns to its start), one per start parity
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    int64_t graph_counts[2][KC_COUNT] = {{0}};
+    bool use_graphs = true;
     // errors
     std::string err;
     bool poisoned = false;
@@ -259,31 +264,30 @@ static deblur_status upload_slice(deblur_t h, float *dst, int64_t dpitch, const 
     return DEBLUR_OK;
 }
 
-static std::vector<float> default_x0(const deblur_params *p) {
-    // A6: x0 = u0 = max(0, y edge-replicated into the c-wide margin)
-    const int c = (p->psf_size - 1) / 2;
-    const int64_t my = p->ny - p->psf_size + 1, mx = p->nx - p->psf_size + 1;
-    std::vector<float> x((size_t)(p->ny * p->nx));
-    for (int64_t r = 0; r < p->ny; ++r) {
-        const int64_t yr = std::min<int64_t>(std::max<int64_t>(r - c, 0), my - 1);
-        for (int64_t q = 0; q < p->nx; ++q) {
-            const int64_t yq = std::min<int64_t>(std::max<int64_t>(q - c, 0), mx - 1);
-            x[(size_t)(r * p->nx + q)] = std::max(0.f, p->y[yr * mx + yq]);
+// x0 given: upload its facet slices to x[0] and copy to u.  x0 == NULL: the A6
+// default computed on the device from the observed rows/cols each facet needs.
+static deblur_status upload_state_x0(deblur_t h, const float *x0, const float *y) {
+    const Plan &pl = h->plan;
+    const int c = (pl.P - 1) / 2;
+    float *ydil = nullptr;
+    for (size_t li = 0; li < h->local.size(); ++li) {
+        const FacetPlan &fp = pl.facets[h->local[li]];
+        FacetDev &F = h->fh[li];
+        if (x0) {
+            deblur_status s = upload_slice(h, F.x[0], F.ep, x0, pl.nx, fp.ey0, fp.ex0, F.ny, F.nx);
+            if (s != DEBLUR_OK) return s;
+            CU(cudaMemcpy2DAsync(F.u, F.ep * 4, F.x[0], F.ep * 4, F.nx * 4, F.ny, cudaMemcpyDeviceToDevice, h->stream));
+        } else {
+            const int64_t y0 = std::max<int64_t>(0, fp.ey0 - c), y1 = std::min<int64_t>(pl.my, fp.ey1 - c);
+            const int64_t x0c = std::max<int64_t>(0, fp.ex0 - c), x1 = std::min<int64_t>(pl.mx, fp.ex1 - c);
+            const int64_t w = x1 - x0c, hh = y1 - y0;
+            if (!ydil) CU(cudaMallocAsync((void **)&ydil, (size_t)(pl.my + 2) * (pl.mx + 2) * 4, h->stream));
+            CU(cudaMemcpy2DAsync(ydil, w * 4, y + y0 * pl.mx + x0c, pl.mx * 4, w * 4, hh, cudaMemcpyHostToDevice,
+                                 h->stream));
+            CU(launch_x0_from_y(F, ydil, w, (int)y0, (int)x0c, (int)pl.my, (int)pl.mx, c, h->stream));
         }
     }
-    return x;
-}
-
-static deblur_status upload_state_x0(deblur_t h, const float *x0) {
-    std::vector<float> tmp;
-    if (!x0) { tmp = default_x0(&h->prm); x0 = tmp.data(); }
-    for (size_t li = 0; li < h->local.size(); ++li) {
-        const FacetPlan &fp = h->plan.facets[h->local[li]];
-        FacetDev &F = h->fh[li];
-        deblur_status s;
-        if ((s = upload_slice(h, F.x[0], F.ep, x0, h->plan.nx, fp.ey0, fp.ex0, F.ny, F.nx)) != DEBLUR_OK) return s;
-        if ((s = upload_slice(h, F.u, F.ep, x0, h->plan.nx, fp.ey0, fp.ex0, F.ny, F.nx)) != DEBLUR_OK) return s;
-    }
+    if (ydil) CU(cudaFreeAsync(ydil, h->stream));
     h->par = 0;
     CU(cudaStreamSynchronize(h->stream));
     return DEBLUR_OK;
@@ -447,6 +451,8 @@ deblur_status deblur_destroy(deblur_t h) {
     if (!h) return DEBLUR_OK;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
+    for (auto &g : h->gexec)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
     if (h->fft) { fft_destroy(h->fft); h->fft = nullptr; }
     if (h->comm) { ncclCommDestroy(h->comm); h->comm = nullptr; }
     for (auto &p : h->pending) { h->ev_pool.push_back(p.a); h->ev_pool.push_back(p.b); }
@@ -468,6 +474,7 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
     deblur_t h = hp.get();
     h->prm = *p;
     h->rank = p->rank; h->world = p->world; h->device = p->device;
+    if (const char *ng = std::getenv("DEBLUR_NO_GRAPHS")) h->use_graphs = (ng[0] == '0');
     err = make_plan(p->ny, p->nx, p->psf_size, p->facet_gy, p->facet_gx, p->overlap, p->world, h->plan);
     if (!err.empty()) { g_last_error = err; return DEBLUR_ESHAPE; }
     const Plan &pl = h->plan;
@@ -659,7 +666,7 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
     // data + initial state
     st = upload_y(h, p->y);
     if (st != DEBLUR_OK) { g_last_error = h->err; return st; }
-    st = upload_state_x0(h, p->x0);
+    st = upload_state_x0(h, p->x0, p->y);
     if (st != DEBLUR_OK) { g_last_error = h->err; return st; }
 
     // FFT path plan
@@ -685,19 +692,54 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
     return DEBLUR_OK;
 }
 
+static deblur_status one_iteration(deblur_t h) {
+    deblur_status s;
+    for (int k = 0; k < h->prm.inner_steps; ++k)
+        if ((s = local_step(h, k == h->prm.inner_steps - 1)) != DEBLUR_OK) return s;
+    if ((s = exchange(h, 0)) != DEBLUR_OK) return s;
+    cudaEvent_t ev = nullptr;
+    h->prof_begin(KC_CONSENSUS, &ev);
+    CU(launch_consensus(h->d_facets, h->d_rects, (int)h->rects.size(), h->par, h->sc.rho, h->stream));
+    h->prof_end(KC_CONSENSUS, ev);
+    return DEBLUR_OK;
+}
+
+// Capture two iterations starting at the current parity into a CUDA graph (the
+// launch-bound small configs spend most of a step in launch latency otherwise).
+static deblur_status capture_pair(deblur_t h) {
+    const int p0 = h->par;
+    int64_t before[KC_COUNT];
+    std::copy(h->stat_n, h->stat_n + KC_COUNT, before);
+    CU(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeRelaxed));
+    deblur_status s = one_iteration(h);
+    if (s == DEBLUR_OK) s = one_iteration(h);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+    if (s != DEBLUR_OK) { if (g) cudaGraphDestroy(g); return s; }
+    if (e != cudaSuccess) return h->cuda_fail(e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&h->gexec[p0], g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return h->cuda_fail(e, "cudaGraphInstantiate");
+    for (int i = 0; i < KC_COUNT; ++i) { h->graph_counts[p0][i] = h->stat_n[i] - before[i]; h->stat_n[i] = before[i]; }
+    h->par = p0;     // 2 iterations flip the parity an even number of times
+    return DEBLUR_OK;
+}
+
 deblur_status deblur_iterate(deblur_t h, int32_t n) {
     deblur_status s = check_state(h);
     if (s != DEBLUR_OK) return s;
     if (n < 0) return h->fail(DEBLUR_EINVAL, "n must be >= 0");
-    for (int it = 0; it < n; ++it) {
-        for (int k = 0; k < h->prm.inner_steps; ++k)
-            if ((s = local_step(h, k == h->prm.inner_steps - 1)) != DEBLUR_OK) return s;
-        if ((s = exchange(h, 0)) != DEBLUR_OK) return s;
-        cudaEvent_t ev = nullptr;
-        h->prof_begin(KC_CONSENSUS, &ev);
-        CU(launch_consensus(h->d_facets, h->d_rects, (int)h->rects.size(), h->par, h->sc.rho, h->stream));
-        h->prof_end(KC_CONSENSUS, ev);
+    int done = 0;
+    if (!h->prof && h->use_graphs && n >= 2) {
+        const int p0 = h->par;
+        if (!h->gexec[p0] && (s = capture_pair(h)) != DEBLUR_OK) return s;
+        for (; done + 2 <= n; done += 2) {
+            CU(cudaGraphLaunch(h->gexec[p0], h->stream));
+            for (int i = 0; i < KC_COUNT; ++i) h->stat_n[i] += h->graph_counts[p0][i];
+        }
     }
+    for (; done < n; ++done)
+        if ((s = one_iteration(h)) != DEBLUR_OK) return s;
     return finish(h);
 }
 
@@ -976,6 +1018,15 @@ deblur_status deblur_get_image(deblur_t h, float *x) {
     if (s != DEBLUR_OK) return s;
     const Plan &pl = h->plan;
     if (h->rank == 0 && !x) return h->fail(DEBLUR_EINVAL, "x is NULL on rank 0");
+    if (h->world == 1) {       // blend on the device in facet order, one D2H copy
+        float *img = nullptr;
+        CU(cudaMallocAsync((void **)&img, (size_t)pl.ny * pl.nx * 4, h->stream));
+        CU(cudaMemsetAsync(img, 0, (size_t)pl.ny * pl.nx * 4, h->stream));
+        for (size_t li = 0; li < h->local.size(); ++li) CU(launch_blend(h->fh[li], h->par, img, pl.nx, h->stream));
+        CU(cudaMemcpyAsync(x, img, (size_t)pl.ny * pl.nx * 4, cudaMemcpyDeviceToHost, h->stream));
+        CU(cudaFreeAsync(img, h->stream));
+        return finish(h);
+    }
     // gather every facet's x to rank 0, then x_hat = sum_f omega^F_f x_f in facet order (A7)
     int64_t n = 0;
     deblur_state_size(h, &n);
@@ -1016,13 +1067,7 @@ deblur_status deblur_reset(deblur_t h, const float *y, const float *x0) {
     if (s != DEBLUR_OK) return s;
     if (!y) return h->fail(DEBLUR_EINVAL, "y is NULL");
     if ((s = upload_y(h, y)) != DEBLUR_OK) return s;
-    if (!x0) {
-        deblur_params p = h->prm;
-        p.y = y;
-        std::vector<float> x = default_x0(&p);
-        return upload_state_x0(h, x.data());
-    }
-    return upload_state_x0(h, x0);
+    return upload_state_x0(h, x0, y);
 }
 
 deblur_status deblur_get_step(deblur_t h, double *tau) {

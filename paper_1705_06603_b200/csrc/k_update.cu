@@ -210,7 +210,43 @@ __global__ void __launch_bounds__(256) k_maxdiff(const FacetDev *facets, const B
     }
 }
 
+// A6 default start: x0 = u0 = max(0, y edge-replicated into the c-wide margin),
+// from a device copy of the observed rows/cols the facet needs (origin (dy0, dx0)).
+__global__ void k_x0_from_y(FacetDev F, const float *ydil, int64_t dpitch, int dy0, int dx0, int My, int Mx, int c) {
+    const int64_t n = (int64_t)F.ny * F.nx;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(idx / F.nx), q = (int)(idx % F.nx);
+        const int yr = min(max(F.ey0 + r - c, 0), My - 1), yq = min(max(F.ex0 + q - c, 0), Mx - 1);
+        const float v = fmaxf(0.f, ydil[(int64_t)(yr - dy0) * dpitch + (yq - dx0)]);
+        const int64_t o = (int64_t)r * F.ep + q;
+        F.x[0][o] = v;
+        F.u[o] = v;
+    }
+}
+
+// image += omega^F_f . x_f over the facet's estimate block (A7); launched per facet in id order
+__global__ void k_blend(FacetDev F, int par, float *img, int64_t Nx) {
+    const int64_t n = (int64_t)F.ny * F.nx;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(idx / F.nx), q = (int)(idx % F.nx);
+        const float om = omega_axis(F.ay, r) * omega_axis(F.ax, q);
+        float *d = img + (int64_t)(F.ey0 + r) * Nx + F.ex0 + q;
+        *d += om * F.x[par][(int64_t)r * F.ep + q];
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_x0_from_y(const FacetDev &F, const float *ydil, int64_t dpitch, int dy0, int dx0, int My, int Mx,
+                             int c, cudaStream_t s) {
+    k_x0_from_y<<<1184, 256, 0, s>>>(F, ydil, dpitch, dy0, dx0, My, Mx, c);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_blend(const FacetDev &F, int par, float *img, int64_t Nx, cudaStream_t s) {
+    k_blend<<<1184, 256, 0, s>>>(F, par, img, Nx);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_update_from_g(const FacetDev *facets, const TileDesc *tiles, int ntiles, int, int par, int last,
                                  const SolverConst &sc, double *partials, cudaStream_t s) {

@@ -42,4 +42,8 @@ cudaError_t launch_tv_value(const FacetDev *facets, const TileDesc *tiles, int n
 cudaError_t launch_maxdiff(const FacetDev *facets, const BandRect *rects, int nrect, int par, double *partials,
                            cudaStream_t s);
 
+cudaError_t launch_x0_from_y(const FacetDev &F, const float *ydil, int64_t dpitch, int dy0, int dx0, int My, int Mx,
+                             int c, cudaStream_t s);
+cudaError_t launch_blend(const FacetDev &F, int par, float *img, int64_t Nx, cudaStream_t s);
+
 }  // namespace deblur

@@ -240,3 +240,23 @@ def test_kernel_work_counts():
         w = dev.kernel_work()
     assert w["H_direct_residual"][0] == pytest.approx(fl_h, rel=1e-12)
     assert w["HT_direct_update"][0] == pytest.approx(fl_ht, rel=1e-12)
+
+
+@pytest.mark.parametrize("path", PATHS, ids=["direct", "fft"])
+def test_reset_default_init_and_image(path):
+    """deblur_reset(y) restarts from the A6 default (computed on the device) and
+    get_image blends the facets (A7); both equal the oracle's definitions."""
+    pb = synth.make_config(2, n=300, facets=(3, 2), overlap=40)
+    y2 = (pb.y[::-1, :] * 1.5 - 0.01).astype(np.float32)      # a different observation, some negatives
+    with D.Deblur.from_problem(pb, conv_path=path) as dev:
+        dev.iterate(3)
+        dev.reset(y2)
+        xs, us = dev.get_state()
+        img = dev.get_image()
+    pb2 = synth.make_config(2, n=300, facets=(3, 2), overlap=40)
+    pb2.y = y2
+    orc = from_problem(pb2)
+    xr, ur = orc.state()
+    np.testing.assert_array_equal(xs, xr.astype(np.float32))
+    np.testing.assert_array_equal(us, ur.astype(np.float32))
+    assert rel_l2(img, orc.image()) <= 1e-6
