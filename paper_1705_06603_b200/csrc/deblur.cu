@@ -85,6 +85,9 @@ struct deblur_ctx {
     std::vector<cudaEvent_t> ev_pool;
     int64_t stat_n[KC_COUNT] = {0};
     double stat_ms[KC_COUNT] = {0};
+    // persistent staging buffers for reset / get_image (allocated on first use)
+    float *d_ystage = nullptr;
+    float *d_image = nullptr;
     // CUDA graphs of two full iterations (parity returns to its start), one per start parity
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     int64_t graph_counts[2][KC_COUNT] = {{0}};
@@ -281,13 +284,13 @@ static deblur_status upload_state_x0(deblur_t h, const float *x0, const float *y
             const int64_t y0 = std::max<int64_t>(0, fp.ey0 - c), y1 = std::min<int64_t>(pl.my, fp.ey1 - c);
             const int64_t x0c = std::max<int64_t>(0, fp.ex0 - c), x1 = std::min<int64_t>(pl.mx, fp.ex1 - c);
             const int64_t w = x1 - x0c, hh = y1 - y0;
-            if (!ydil) CU(cudaMallocAsync((void **)&ydil, (size_t)(pl.my + 2) * (pl.mx + 2) * 4, h->stream));
+            if (!h->d_ystage) CU(h->dalloc(&h->d_ystage, (size_t)(pl.my + 2) * (pl.mx + 2)));
+            ydil = h->d_ystage;
             CU(cudaMemcpy2DAsync(ydil, w * 4, y + y0 * pl.mx + x0c, pl.mx * 4, w * 4, hh, cudaMemcpyHostToDevice,
                                  h->stream));
             CU(launch_x0_from_y(F, ydil, w, (int)y0, (int)x0c, (int)pl.my, (int)pl.mx, c, h->stream));
         }
     }
-    if (ydil) CU(cudaFreeAsync(ydil, h->stream));
     h->par = 0;
     CU(cudaStreamSynchronize(h->stream));
     return DEBLUR_OK;
@@ -1019,12 +1022,11 @@ deblur_status deblur_get_image(deblur_t h, float *x) {
     const Plan &pl = h->plan;
     if (h->rank == 0 && !x) return h->fail(DEBLUR_EINVAL, "x is NULL on rank 0");
     if (h->world == 1) {       // blend on the device in facet order, one D2H copy
-        float *img = nullptr;
-        CU(cudaMallocAsync((void **)&img, (size_t)pl.ny * pl.nx * 4, h->stream));
+        if (!h->d_image) CU(h->dalloc(&h->d_image, (size_t)pl.ny * pl.nx));
+        float *img = h->d_image;
         CU(cudaMemsetAsync(img, 0, (size_t)pl.ny * pl.nx * 4, h->stream));
         for (size_t li = 0; li < h->local.size(); ++li) CU(launch_blend(h->fh[li], h->par, img, pl.nx, h->stream));
         CU(cudaMemcpyAsync(x, img, (size_t)pl.ny * pl.nx * 4, cudaMemcpyDeviceToHost, h->stream));
-        CU(cudaFreeAsync(img, h->stream));
         return finish(h);
     }
     // gather every facet's x to rank 0, then x_hat = sum_f omega^F_f x_f in facet order (A7)
