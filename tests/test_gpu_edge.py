@@ -62,8 +62,8 @@ def test_image_smaller_than_a_tile(path):
 def test_c5_geometry_shrunk(path):
     """8x8 facets with the c5 PSF family (P = 127, elliptical Moffat grid), shrunk so
     the oracle finishes: facet cores just above O + P - 1."""
-    n = 8 * 200 + 126
-    pb = synth.make_config(5, n=n, overlap=64)
+    n = 8 * 256 + 126                     # facet core 256 >= O + P - 1 = 254; O >= P - 1 for apply_HT
+    pb = synth.make_config(5, n=n, overlap=128)
     op = Operator(pb.psfs, pb.wy, pb.wx)
     rng = np.random.default_rng(5)
     x = (0.05 + 0.5 * rng.random((pb.ny, pb.nx))).astype(np.float32)
