@@ -139,13 +139,28 @@ struct Stage {
     template <int SIGN>
     __device__ static __forceinline__ void bfly(float2 *v, int j, const float2 *W, int S) {
         if (Ns > 1) {
+            // w^r for r = 1..R-1: w, w^2, w^4 from the fp64-built table, the rest by at
+            // most two products (<= ~2 ulp), saving shared-memory loads (the column pass
+            // is bound by shared-memory wavefronts)
             const int k = j % Ns;
             const int step = S / (Ns * R);
+            float2 w[8];
+            w[1] = W[(k * step) & (S - 1)];
+            if (R >= 4) {
+                w[2] = W[(2 * k * step) & (S - 1)];
+                w[3] = cmul(w[1], w[2]);
+            }
+            if (R == 8) {
+                w[4] = W[(4 * k * step) & (S - 1)];
+                w[5] = cmul(w[4], w[1]);
+                w[6] = cmul(w[4], w[2]);
+                w[7] = cmul(w[4], w[3]);
+            }
 #pragma unroll
             for (int r = 1; r < R; ++r) {
-                float2 w = W[(k * r * step) & (S - 1)];
-                if (SIGN > 0) w.y = -w.y;
-                v[r] = cmul(v[r], w);
+                float2 ww = w[r];
+                if (SIGN > 0) ww.y = -ww.y;
+                v[r] = cmul(v[r], ww);
             }
         }
         if (R == 8) dft8<SIGN>(v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7]);
