@@ -73,27 +73,35 @@ __device__ __forceinline__ float update_pixel(const FacetDev &F, const float *xh
 }
 
 // Same arithmetic as update_pixel, returning x+ and the dual/band values instead of
-// storing them (the caller vectorises the stores).  phi is computed only when asked.
-__device__ __forceinline__ float update_value(const FacetDev &F, const float *xh, int XH, int i, int j, int fy, int fx,
-                                              float g, float uc, const SolverConst &sc, bool want_phi, float &phi,
-                                              int last, bool &shared, float &u_new, float &v_new) {
-    const int ny = F.ny, nx = F.nx;
-    const bool neu = sc.tv_boundary == 1;
+// storing them (the caller vectorises the stores).  Compile-time regulariser / D
+// boundary (REG: 0 smoothed TV, 1 Huber; NEU: Neumann) keep the hot loop branch-free;
+// phi is computed only when asked.
+template <int REG, bool NEU>
+__device__ __forceinline__ float update_value_t(const FacetDev &F, const float *xh, int XH, int i, int j, int fy,
+                                                int fx, float g, float uc, const SolverConst &sc, bool want_phi,
+                                                float &phi, bool &shared, float &u_new, float &v_new) {
     const float e2 = sc.eps * sc.eps;
     auto X = [&](int a, int b) { return xh[a * XH + b]; };
-    const int fyu = (fy == 0) ? ny - 1 : fy - 1;
-    const int fxl = (fx == 0) ? nx - 1 : fx - 1;
     const float xc = X(i, j);
-    const float dyc = (neu && fy == ny - 1) ? 0.f : X(i + 1, j) - xc;
-    const float dxc = (neu && fx == nx - 1) ? 0.f : X(i, j + 1) - xc;
-    const float dyu = (neu && fyu == ny - 1) ? 0.f : xc - X(i - 1, j);
-    const float dxu = (neu && fx == nx - 1) ? 0.f : X(i - 1, j + 1) - X(i - 1, j);
-    const float dyl = (neu && fy == ny - 1) ? 0.f : X(i + 1, j - 1) - X(i, j - 1);
-    const float dxl = (neu && fxl == nx - 1) ? 0.f : xc - X(i, j - 1);
+    float dyc = X(i + 1, j) - xc;
+    float dxc = X(i, j + 1) - xc;
+    float dyu = xc - X(i - 1, j);
+    float dxu = X(i - 1, j + 1) - X(i - 1, j);
+    float dyl = X(i + 1, j - 1) - X(i, j - 1);
+    float dxl = xc - X(i, j - 1);
+    if (NEU) {
+        const int ny = F.ny, nx = F.nx;
+        const int fyu = (fy == 0) ? ny - 1 : fy - 1;
+        const int fxl = (fx == 0) ? nx - 1 : fx - 1;
+        if (fy == ny - 1) { dyc = 0.f; dyl = 0.f; }
+        if (fx == nx - 1) { dxc = 0.f; dxu = 0.f; }
+        if (fyu == ny - 1) dyu = 0.f;
+        if (fxl == nx - 1) dxl = 0.f;
+    }
     float sc_c, sc_u, sc_l;
     const float t2c = dyc * dyc + dxc * dxc;
     phi = 0.f;
-    if (sc.reg_kind == 0) {
+    if (REG == 0) {
         sc_c = rsqrtf(t2c + e2);
         sc_u = rsqrtf(dyu * dyu + dxu * dxu + e2);
         sc_l = rsqrtf(dyl * dyl + dxl * dxl + e2);
@@ -107,13 +115,12 @@ __device__ __forceinline__ float update_value(const FacetDev &F, const float *xh
         if (want_phi) phi = (tc <= d) ? 0.5f * t2c : d * (tc - 0.5f * d);
     }
     const float tdiv = dyu * sc_u - dyc * sc_c + dxl * sc_l - dxc * sc_c;
-    const float om = omega_axis(F.ay, fy) * omega_axis(F.ax, fx);
+    shared = fy < F.ay.b_prev || fy >= F.ay.b_next || fx < F.ax.b_prev || fx >= F.ax.b_next;
+    const float om = shared ? omega_axis(F.ay, fy) * omega_axis(F.ax, fx) : 1.f;
     const float gt = g + sc.lambda * tdiv + sc.gamma * om * (xc - uc);
     const float xn = fmaxf(0.f, xc - sc.tau * gt);
-    shared = fy < F.ay.b_prev || fy >= F.ay.b_next || fx < F.ax.b_prev || fx >= F.ax.b_next;
     u_new = uc + sc.rho * (xn - uc);
     v_new = 2.f * xn - uc;
-    (void)last;
     return xn;
 }
 

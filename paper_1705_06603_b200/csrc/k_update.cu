@@ -21,6 +21,7 @@ constexpr int UT_TY = 32, UT_TX = 128;   // update tile (matches the H^T tile gr
 // K4: tile of UT_TY x UT_TX pixels; each thread owns a 4-pixel strip in 4 rows.
 // x halo staged with 16-byte loads (interior tiles) or a wrapped scalar path
 // (tiles touching the facet border: circular D within the facet, A2).
+template <int REG, bool NEU>
 __global__ void __launch_bounds__(EPI_NT) k_update_from_g(const FacetDev *facets, const TileDesc *tiles, int par,
                                                            int last, SolverConst sc, double *partials) {
     constexpr int XH = UT_TX + 8;                    // smem col c <-> facet col x0 - 4 + c
@@ -89,8 +90,8 @@ __global__ void __launch_bounds__(EPI_NT) k_update_from_g(const FacetDev *facets
         for (int j = 0; j < 4; ++j) {
             const int fx = fx0 + j;
             float phi;
-            xn[j] = update_value(F, xh, XH, ly + 1, lx0 + j + 4, fy, fx, gv[k][j], uv[k][j], sc, partials != nullptr,
-                                 phi, last, sh[j], nu[j], nv[j]);
+            xn[j] = update_value_t<REG, NEU>(F, xh, XH, ly + 1, lx0 + j + 4, fy, fx, gv[k][j], uv[k][j], sc,
+                                             partials != nullptr, phi, sh[j], nu[j], nv[j]);
             if (fx < F.nx) rsum += (double)phi;
         }
         if (full) {
@@ -251,7 +252,14 @@ cudaError_t launch_blend(const FacetDev &F, int par, float *img, int64_t Nx, cud
 cudaError_t launch_update_from_g(const FacetDev *facets, const TileDesc *tiles, int ntiles, int, int par, int last,
                                  const SolverConst &sc, double *partials, cudaStream_t s) {
     if (!ntiles) return cudaSuccess;
-    k_update_from_g<<<ntiles, EPI_NT, 0, s>>>(facets, tiles, par, last, sc, partials);
+    if (sc.reg_kind == 0 && sc.tv_boundary == 0)
+        k_update_from_g<0, false><<<ntiles, EPI_NT, 0, s>>>(facets, tiles, par, last, sc, partials);
+    else if (sc.reg_kind == 0)
+        k_update_from_g<0, true><<<ntiles, EPI_NT, 0, s>>>(facets, tiles, par, last, sc, partials);
+    else if (sc.tv_boundary == 0)
+        k_update_from_g<1, false><<<ntiles, EPI_NT, 0, s>>>(facets, tiles, par, last, sc, partials);
+    else
+        k_update_from_g<1, true><<<ntiles, EPI_NT, 0, s>>>(facets, tiles, par, last, sc, partials);
     return cudaGetLastError();
 }
 
