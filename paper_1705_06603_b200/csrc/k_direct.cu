@@ -56,6 +56,30 @@ __device__ __forceinline__ void fma_block(float (&part)[RY][8], const float (&xa
     }
 }
 
+// Same as fma_block when every tap row a = s - ry (ry < RY) is valid: no branches, so
+// all 2*RY tap loads and the window loads can be issued ahead of the FFMAs.
+template <int RY>
+__device__ __forceinline__ void fma_block_full(float (&part)[RY][8], const float (&xa)[12], const float (&xb)[12],
+                                               const float *__restrict__ hs, int Pp, int s, int cb) {
+    float hh[RY][8];
+#pragma unroll
+    for (int ry = 0; ry < RY; ++ry) {
+        const float4 h0 = *reinterpret_cast<const float4 *>(hs + (s - ry) * Pp + cb);
+        const float4 h1 = *reinterpret_cast<const float4 *>(hs + (s - ry) * Pp + cb + 4);
+        hh[ry][0] = h0.x; hh[ry][1] = h0.y; hh[ry][2] = h0.z; hh[ry][3] = h0.w;
+        hh[ry][4] = h1.x; hh[ry][5] = h1.y; hh[ry][6] = h1.z; hh[ry][7] = h1.w;
+    }
+#pragma unroll
+    for (int ry = 0; ry < RY; ++ry)
+#pragma unroll
+        for (int bb = 0; bb < 8; ++bb)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                part[ry][j] = fmaf(hh[ry][bb], xa[j + bb], part[ry][j]);
+                part[ry][4 + j] = fmaf(hh[ry][bb], xb[j + bb], part[ry][4 + j]);
+            }
+}
+
 __device__ __forceinline__ void load12(float (&w)[12], const float *p) {
     const float4 a = *reinterpret_cast<const float4 *>(p);
     const float4 b = *reinterpret_cast<const float4 *>(p + 4);
@@ -138,11 +162,20 @@ __global__ void __launch_bounds__(NT) k_H_direct(ConvArgs A, int mode, int par) 
 #pragma unroll
                     for (int j = 0; j < 8; ++j) part[i][j] = 0.f;
                 const float *xr = xs + (ty * RY + s) * XP + tx * 4;
-                for (int cb = 0; cb < Pp; cb += 8) {
-                    float xa[12], xb[12];
-                    load12(xa, xr + cb);
-                    load12(xb, xr + 64 + cb);
-                    fma_block<RY>(part, xa, xb, hs, Pp, P, s, cb);
+                if (s >= RY - 1 && s < P) {          // bulk: every tap row valid
+                    for (int cb = 0; cb < Pp; cb += 8) {
+                        float xa[12], xb[12];
+                        load12(xa, xr + cb);
+                        load12(xb, xr + 64 + cb);
+                        fma_block_full<RY>(part, xa, xb, hs, Pp, s, cb);
+                    }
+                } else {
+                    for (int cb = 0; cb < Pp; cb += 8) {
+                        float xa[12], xb[12];
+                        load12(xa, xr + cb);
+                        load12(xb, xr + 64 + cb);
+                        fma_block<RY>(part, xa, xb, hs, Pp, P, s, cb);
+                    }
                 }
 #pragma unroll
                 for (int ry = 0; ry < RY; ++ry) {
@@ -264,11 +297,20 @@ __global__ void __launch_bounds__(NT) k_HT_direct(ConvArgs A, int mode, int par,
 #pragma unroll
                     for (int j = 0; j < 8; ++j) part[i][j] = 0.f;
                 const float *xr = rs + (ty * RY + s) * XP + tx * 4;
-                for (int cb = 0; cb < Pp; cb += 8) {
-                    float xa[12], xb[12];
-                    load12(xa, xr + cb);
-                    load12(xb, xr + 64 + cb);
-                    fma_block<RY>(part, xa, xb, hs, Pp, P, s, cb);
+                if (s >= RY - 1 && s < P) {
+                    for (int cb = 0; cb < Pp; cb += 8) {
+                        float xa[12], xb[12];
+                        load12(xa, xr + cb);
+                        load12(xb, xr + 64 + cb);
+                        fma_block_full<RY>(part, xa, xb, hs, Pp, s, cb);
+                    }
+                } else {
+                    for (int cb = 0; cb < Pp; cb += 8) {
+                        float xa[12], xb[12];
+                        load12(xa, xr + cb);
+                        load12(xb, xr + 64 + cb);
+                        fma_block<RY>(part, xa, xb, hs, Pp, P, s, cb);
+                    }
                 }
 #pragma unroll
                 for (int ry = 0; ry < RY; ++ry) {
