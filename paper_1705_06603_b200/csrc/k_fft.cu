@@ -49,6 +49,7 @@ struct FftArgs {
     float2 *scratch;        // per tile: tile_rows x LDF
     int64_t tile_rows;      // rows of LDF complex per tile
     int NQ;                 // q slots per tile
+    int NP;                 // max active p per tile (wy rows staged per CTA)
     double *partials;
     float scale;            // 2 / S^2
 };
@@ -381,16 +382,17 @@ __global__ void __launch_bounds__(GC<S>::NTH) k_cols(FftArgs A, int mode, const 
     float2 *hbuf = Wsm + S;          // S x NB (prefetched PSF spectrum chunk)
     float2 *colq = hbuf + S * NB;    // NB x CS
     float2 *work = colq + NB * CS;   // NB x CS
-    float *wys = reinterpret_cast<float *>(work + NB * CS);   // S
+    float *wys_all = reinterpret_cast<float *>(work + NB * CS);   // NP x S: every active wy_p of the tile
+    int *slot_s = reinterpret_cast<int *>(wys_all + (size_t)A.NP * S);   // NP x NQ PSF-spectrum slots
     const int tid = threadIdx.x;
     const int nchunk = (NF + NB - 1) / NB;
     const int tile = blockIdx.x / nchunk, f0 = (blockIdx.x % nchunk) * NB;
     const int P = A.P, c2 = P - 1, T = S - P + 1;
     for (int i = tid; i < S; i += NTH) Wsm[i] = A.W[i];
-    __syncthreads();
     float2 v[E];
 
     if (mode == 2) {
+        __syncthreads();
         if (tile >= npsf) return;
         const float2 *src = hrows + (int64_t)tile * S * LDF + f0;
 #pragma unroll
@@ -416,18 +418,33 @@ __global__ void __launch_bounds__(GC<S>::NTH) k_cols(FftArgs A, int mode, const 
     const TileDesc td = A.tiles[tile];
     const FacetDev &Fd = A.facets[td.f];
     float2 *base = A.scratch + (int64_t)tile * A.tile_rows * LDF;
-    auto hk = [&](int p, int q) { return A.Hhat + (int64_t)A.psf_slot[p * A.Gx + q] * S * LDF + f0; };
-    auto fill_wys = [&](int p) {
-        const float *wyp = A.wy + (size_t)p * A.Ny + Fd.ey0 + td.y0;
-        for (int i = tid; i < S; i += NTH) wys[i] = (td.y0 + i < Fd.ny) ? __ldg(wyp + i) : 0.f;
+    {
+        // stage every active row weight wy_p and PSF slot once per CTA: no global
+        // latency is exposed inside the (p, q) loops
+        const int np = td.p1 - td.p0 + 1, nq = td.q1 - td.q0 + 1;
+        for (int idx = tid; idx < np * S; idx += NTH) {
+            const int pi = idx / S, i = idx - pi * S;
+            wys_all[idx] = (td.y0 + i < Fd.ny) ? __ldg(A.wy + (size_t)(td.p0 + pi) * A.Ny + Fd.ey0 + td.y0 + i) : 0.f;
+        }
+        for (int idx = tid; idx < np * nq; idx += NTH) {
+            const int pi = idx / nq, qi = idx - pi * nq;
+            slot_s[idx] = __ldg(A.psf_slot + (td.p0 + pi) * A.Gx + td.q0 + qi);
+        }
+    }
+    __syncthreads();
+    const int nqt = td.q1 - td.q0 + 1;
+    auto hk = [&](int p, int q) {
+        return A.Hhat + (int64_t)slot_s[(p - td.p0) * nqt + (q - td.q0)] * S * LDF + f0;
     };
+    const float *wys = wys_all;
+    auto fill_wys = [&](int p) { wys = wys_all + (size_t)(p - td.p0) * S; };
 
     if (mode == 0) {
         float2 acc[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) acc[e] = make_float2(0.f, 0.f);
         for (int q = td.q0; q <= td.q1; ++q) {
-            __syncthreads();
+            // (colq is free: every stage-0 read of the previous q precedes a barrier in middle())
             {   // batched load of the row-spectrum chunk of A_q
                 constexpr int LPT = NB * S / NTH;
                 const float2 *Aq = base + (int64_t)(q - td.q0) * S * LDF + f0;
@@ -447,7 +464,6 @@ __global__ void __launch_bounds__(GC<S>::NTH) k_cols(FftArgs A, int mode, const 
                 __syncthreads();
                 prefetch_hhat<S, NB, NTH, LDF>(hbuf, hk(p, q), tid);   // overlaps the FFT below
                 fill_wys(p);
-                __syncthreads();
                 // stage 0 from colq, weighted by the row weight wy_p (constant along the row)
 #pragma unroll
                 for (int i = 0; i < S0::BPT; ++i) {
@@ -518,7 +534,6 @@ __global__ void __launch_bounds__(GC<S>::NTH) k_cols(FftArgs A, int mode, const 
 #pragma unroll
         for (int e = 0; e < E; ++e) acc[e] = make_float2(0.f, 0.f);
         for (int p = td.p0; p <= td.p1; ++p) {
-            __syncthreads();
             fill_wys(p);
             __pipeline_wait_prior(0);
             __syncthreads();
@@ -703,7 +718,7 @@ __global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
 }  // namespace
 
 struct FftPlan {
-    int S = 0, T = 0, P = 0, NQ = 1;
+    int S = 0, T = 0, P = 0, NQ = 1, NP = 1;
     int K = 0, Gx = 1;
     std::vector<TileDesc> tH, tHT;
     TileDesc *d_tH = nullptr, *d_tHT = nullptr;
@@ -728,7 +743,7 @@ struct FftPlan {
         a.ntiles = (int)(ht ? tHT.size() : tH.size());
         a.W = W; a.Hhat = Hhat; a.psf_slot = psf_slot;
         a.wy = wy; a.wx = wx; a.Ny = Ny; a.Nx = Nx; a.P = P; a.Gx = Gx;
-        a.scratch = scratch; a.tile_rows = tile_rows; a.NQ = NQ;
+        a.scratch = scratch; a.tile_rows = tile_rows; a.NQ = NQ; a.NP = NP;
         a.partials = partials;
         a.scale = 2.0f / ((float)S * (float)S);
         return a;
@@ -764,7 +779,10 @@ static size_t smem_rows_fwd() {
     return (size_t)S * 8 + (size_t)G::NB * G::RS * 8 + (size_t)G::NB * G::XS * 4 + (size_t)S * 4;
 }
 template <int S>
-static size_t smem_cols() { using G = GC<S>; return (size_t)S * 8 + (size_t)S * G::NB * 8 + 2 * (size_t)G::NB * G::CS * 8 + (size_t)S * 4; }
+static size_t smem_cols(int NP, int NQ) {
+    using G = GC<S>;
+    return (size_t)S * 8 + (size_t)S * G::NB * 8 + 2 * (size_t)G::NB * G::CS * 8 + (size_t)NP * S * 4 + (size_t)NP * NQ * 4;
+}
 template <int S>
 static size_t smem_rows_inv(int T, bool ht = true) {
     using G = GR<S>;
@@ -772,10 +790,10 @@ static size_t smem_rows_inv(int T, bool ht = true) {
 }
 
 template <int S>
-static cudaError_t setup_attrs(int T) {
+static cudaError_t setup_attrs(int T, int NP, int NQ) {
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(k_rows_fwd<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rows_fwd<S>())) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(k_cols<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cols<S>())) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_cols<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cols<S>(NP, NQ))) != cudaSuccess) return e;
     return cudaFuncSetAttribute(k_rows_inv<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rows_inv<S>(T));
 }
 
@@ -791,7 +809,7 @@ static cudaError_t run_cols(const FftArgs &a, int ntiles, int mode, const float2
                             cudaStream_t s) {
     if (ntiles == 0) return cudaSuccess;
     const int nchunk = (S / 2 + 1 + GC<S>::NB - 1) / GC<S>::NB;
-    k_cols<S><<<ntiles * nchunk, GC<S>::NTH, smem_cols<S>(), s>>>(a, mode, hrows, hhat, npsf);
+    k_cols<S><<<ntiles * nchunk, GC<S>::NTH, smem_cols<S>(a.NP, a.NQ), s>>>(a, mode, hrows, hhat, npsf);
     return cudaGetLastError();
 }
 template <int S>
@@ -836,8 +854,8 @@ static cudaError_t do_geom(int S, int &ldf, int &nb) {
     FFT_DISPATCH(S, return geom<SS>(ldf, nb));
     return cudaSuccess;
 }
-static cudaError_t do_attrs(int S, int T) {
-    FFT_DISPATCH(S, return setup_attrs<SS>(T));
+static cudaError_t do_attrs(int S, int T, int NP, int NQ) {
+    FFT_DISPATCH(S, return setup_attrs<SS>(T, NP, NQ));
     return cudaSuccess;
 }
 
@@ -898,6 +916,7 @@ FftPlan *fft_create(const Plan &pl, const std::vector<int> &local, const std::ve
     for (auto *lst : {&f->tH, &f->tHT})
         for (auto &t : *lst) {
             f->NQ = std::max(f->NQ, t.q1 - t.q0 + 1);
+            f->NP = std::max(f->NP, t.p1 - t.p0 + 1);
             for (int p = t.p0; p <= t.p1; ++p)
                 for (int q = t.q0; q <= t.q1; ++q) used[p * Gx + q] = 1;
         }
@@ -933,7 +952,7 @@ FftPlan *fft_create(const Plan &pl, const std::vector<int> &local, const std::ve
     FC(cudaMemcpy(f->psf_slot, slot.data(), sizeof(int) * f->K, cudaMemcpyHostToDevice));
     FC(cudaMemcpy(f->d_tH, f->tH.data(), sizeof(TileDesc) * f->tH.size(), cudaMemcpyHostToDevice));
     FC(cudaMemcpy(f->d_tHT, f->tHT.data(), sizeof(TileDesc) * f->tHT.size(), cudaMemcpyHostToDevice));
-    FC(do_attrs(S, T));
+    FC(do_attrs(S, T, f->NP, f->NQ));
     // PSF spectra Hhat_k = DFT2(h_k zero-padded to S x S), for every PSF a local tile touches
     if (!psf_ids.empty()) {
         float *d_sel = nullptr;
