@@ -194,20 +194,26 @@ def run_ours(args, rank, world, local):
     # end to end through the C ABI with host buffers: reset(y from pinned host) + K iterations + image D2H
     y_pin = torch.from_numpy(pb.y).pin_memory()
     img_pin = torch.empty((pb.ny, pb.nx), dtype=torch.float32).pin_memory() if rank == 0 else None
-    barrier()
-    t0 = time.perf_counter()
-    dev.reset(y_pin.numpy())                      # pinned host buffer, no staging copy
-    dev.iterate(args.steps)
-    dev.get_image(out=img_pin.numpy() if img_pin is not None else None)
-    barrier()
-    te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+
+    def e2e_job():
+        barrier()
+        t0 = time.perf_counter()
+        dev.reset(y_pin.numpy())                      # pinned host buffer, no staging copy
+        dev.iterate(args.steps)
+        dev.get_image(out=img_pin.numpy() if img_pin is not None else None)
+        barrier()
+        return time.perf_counter() - t0
+
+    e2e_job()                                         # one untimed job (first-touch of pinned pages)
+    te = torch.tensor([statistics.median(e2e_job() for _ in range(3))], dtype=torch.float64)
     if world > 1:
         import torch.distributed as dist
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e = {"value": round(npix * args.steps / float(te.item()) / 1e6, 3), "unit": "Mpixel-iterations/s",
            "h2d_bytes_per_step": int(pb.y.nbytes // args.steps),
            "d2h_bytes_per_step": int(npix * 4 // args.steps),
-           "job": f"deblur_reset(y host pinned) + deblur_iterate({args.steps}) + deblur_get_image(host pinned)",
+           "job": f"deblur_reset(y host pinned) + deblur_iterate({args.steps}) + deblur_get_image(host pinned); "
+                  "median of 3 jobs after one untimed job",
            "seconds": round(float(te.item()), 3)}
 
     cpu = None

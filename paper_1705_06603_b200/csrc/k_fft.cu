@@ -583,64 +583,60 @@ __global__ void __launch_bounds__(GC<S>::NTH) k_cols(FftArgs A, int mode, const 
 }
 
 // ------------------------------------------------------------------ pass C / C'
-// C2R of NB spectrum rows (global, row stride LDF, rows >= nrows read as zero) into
-// smem reals outs[rr*XS + m] (unscaled: SH x the signal).
+// C2R of NB spectrum rows per CTA.  The rows (global, stride LDF) are streamed into a
+// shared staging buffer with cp.async one source ahead, so the next source's loads
+// are in flight under the current source's FFT.
 template <int S>
-__device__ __forceinline__ void c2r_rows(const float2 *__restrict__ src0, int nrows, float2 *work, float *outs,
-                                         const float2 *Wsm) {
+struct C2R {
     using G = GR<S>;
     using F = typename G::F;
-    constexpr int NB = G::NB, SH = G::SH, RS = G::RS, XS = G::XS, LDF = LD<S>::LDF;
-    const int tid = threadIdx.x;
-    constexpr int LPT = NB * SH / G::NTH;
-    float2 xk[LPT], xc[LPT];
-#pragma unroll
-    for (int it = 0; it < LPT; ++it) {
-        const int idx = tid + it * G::NTH, rr = idx / SH, k = idx % SH;
-        if (rr < nrows) {
-            const float2 *X = src0 + (int64_t)rr * LDF;
-            xk[it] = __ldg(X + k);
-            xc[it] = __ldg(X + SH - k);
-        } else {
-            xk[it] = make_float2(0.f, 0.f);
-            xc[it] = make_float2(0.f, 0.f);
+    static constexpr int NB = G::NB, SH = G::SH, RS = G::RS, LDF = LD<S>::LDF;
+    static constexpr int SS = SH + 2;            // staging row stride (float2; 16-byte rows)
+    // rows [0, nrows) of src0 -> stg (16-byte cp.async; rows >= nrows zero-filled)
+    __device__ static __forceinline__ void issue(float2 *stg, const float2 *src0, int nrows, int tid) {
+        constexpr int V = SH / 2;                 // 16-byte vectors per row, + the Nyquist element
+        for (int idx = tid; idx < NB * (V + 1); idx += G::NTH) {
+            const int rr = idx / (V + 1), v = idx - rr * (V + 1);
+            float2 *d = stg + rr * SS + 2 * v;
+            if (rr < nrows) {
+                const float2 *sp = src0 + (int64_t)rr * LDF + 2 * v;
+                if (v < V) __pipeline_memcpy_async(d, sp, 16);
+                else __pipeline_memcpy_async(d, sp, 8);
+            } else {
+                d[0] = make_float2(0.f, 0.f);
+                if (v < V) d[1] = make_float2(0.f, 0.f);
+            }
+        }
+        __pipeline_commit();
+    }
+    // half-length complex input z = E + i O from the staged spectrum rows -> work
+    __device__ static __forceinline__ void pre(float2 *work, const float2 *stg, const float2 *Wsm, int tid) {
+        for (int idx = tid; idx < NB * SH; idx += G::NTH) {
+            const int rr = idx / SH, k = idx - rr * SH;
+            const float2 xk = stg[rr * SS + k];
+            const float2 b = conjf2(stg[rr * SS + SH - k]);
+            const float2 e = make_float2(0.5f * (xk.x + b.x), 0.5f * (xk.y + b.y));
+            const float2 d = make_float2(0.5f * (xk.x - b.x), 0.5f * (xk.y - b.y));
+            const float2 o = cmul(d, conjf2(Wsm[k]));     // O_k
+            work[rr * RS + k] = make_float2(e.x - o.y, e.y + o.x);   // E + i O
         }
     }
-#pragma unroll
-    for (int it = 0; it < LPT; ++it) {
-        const int idx = tid + it * G::NTH, rr = idx / SH, k = idx % SH;
-        const float2 b = conjf2(xc[it]);
-        const float2 e = make_float2(0.5f * (xk[it].x + b.x), 0.5f * (xk[it].y + b.y));
-        const float2 d = make_float2(0.5f * (xk[it].x - b.x), 0.5f * (xk[it].y - b.y));
-        const float2 o = cmul(d, conjf2(Wsm[k]));     // O_k
-        work[rr * RS + k] = make_float2(e.x - o.y, e.y + o.x);   // E + i O
-    }
-    __syncthreads();
-    float2 v[G::E];
-    F::First::template load_bfly<+1>(work, v, tid, Wsm, S);
-    __syncthreads();
-    F::template middle<+1>(work, v, tid, Wsm, S);
-    using SL = typename F::Last;
-#pragma unroll
-    for (int i = 0; i < SL::BPT; ++i) {
-        int t, j;
-        SL::bj(i, tid, t, j);
-#pragma unroll
-        for (int r = 0; r < SL::R; ++r)
-            *reinterpret_cast<float2 *>(outs + t * XS + 2 * SL::out_n(j, r)) = v[i * SL::R + r];
-    }
-    __syncthreads();
-}
+};
 
-template <int S>
+template <int S, bool HT>
 __global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
     using G = GR<S>;
-    constexpr int NB = G::NB, RS = G::RS, XS = G::XS, LDF = LD<S>::LDF;
+    using C = C2R<S>;
+    using F = typename G::F;
+    using SL = typename F::Last;
+    constexpr int NB = G::NB, RS = G::RS, XS = G::XS, LDF = LD<S>::LDF, E = G::E;
+    static_assert(XS == 2 * RS, "outs aliases work");
     extern __shared__ __align__(16) float2 sm2[];
     float2 *Wsm = sm2;
-    float2 *work = Wsm + S;
-    float *outs = reinterpret_cast<float *>(work + NB * RS);   // NB x XS
-    float *gacc = outs + NB * XS;                              // NB x T (H^T)
+    float2 *work = Wsm + S;                                    // NB x RS; reused as outs (NB x XS reals)
+    float2 *stg = work + NB * RS;                              // NB x SS staging
+    float *wxs = reinterpret_cast<float *>(stg + NB * C::SS);  // NQ x S (H^T)
+    float *outs = reinterpret_cast<float *>(work);
     __shared__ double red[256 / 32];
     const int tid = threadIdx.x;
     const int P = A.P, c2 = P - 1, T = S - P + 1;
@@ -651,67 +647,109 @@ __global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
     const FacetDev &Fd = A.facets[t.f];
     const float2 *base = A.scratch + (int64_t)tile * A.tile_rows * LDF;
     const float scale = A.scale;
+    constexpr bool ht = HT;
+    const int nq = ht ? t.q1 - t.q0 + 1 : 1;
+    const float2 *Bbase = base + (int64_t)S * LDF;
+    auto src = [&](int qi) {
+        return ht ? Bbase + ((int64_t)qi * T + r0) * LDF : base + ((int64_t)A.NQ * S + r0) * LDF;
+    };
+    if (nq > 0) C::issue(stg, src(0), nrows, tid);
     for (int i = tid; i < S; i += G::NTH) Wsm[i] = A.W[i];
-    __syncthreads();
-
-    if (mode != INV_HT) {
-        c2r_rows<S>(base + ((int64_t)A.NQ * S + r0) * LDF, nrows, work, outs, Wsm);
-        double dsum = 0.0;
-        constexpr int U = 8;
-        const int ntot = nrows * T;
-        for (int b0 = 0; b0 < ntot; b0 += U * G::NTH) {
-            float yv[U], wv[U];
-            int64_t off[U];
-            bool ok[U];
+    if (ht) {
+        for (int idx = tid; idx < nq * S; idx += G::NTH) {
+            const int qi = idx / S, cc = idx - qi * S;
+            wxs[idx] = (cc < T && t.x0 + cc < Fd.nx) ? __ldg(A.wx + (size_t)(t.q0 + qi) * A.Nx + Fd.ex0 + t.x0 + cc) : 0.f;
+        }
+    }
+    float2 acc[HT ? E : 1];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int idx = b0 + tid + u * G::NTH;
-                const int rr = idx / T, cc = idx - rr * T;
-                const int oi = t.y0 + r0 + rr, oj = t.x0 + cc;
-                ok[u] = idx < ntot && oi < Fd.my && oj < Fd.mx;
-                off[u] = (int64_t)oi * Fd.op + oj;
-                yv[u] = (ok[u] && mode != FFT_PLAIN) ? __ldg(Fd.y + off[u]) : 0.f;
-                wv[u] = (ok[u] && mode != FFT_PLAIN) ? (Fd.w ? __ldg(Fd.w + off[u]) : Fd.w_scalar) : 0.f;
-            }
+    for (int e = 0; e < (HT ? E : 1); ++e) acc[e] = make_float2(0.f, 0.f);
+    float2 v[E];
+    for (int qi = 0; qi < nq; ++qi) {
+        __pipeline_wait_prior(0);
+        __syncthreads();
+        C::pre(work, stg, Wsm, tid);
+        __syncthreads();
+        if (qi + 1 < nq) C::issue(stg, src(qi + 1), nrows, tid);   // in flight under this FFT
+        F::First::template load_bfly<+1>(work, v, tid, Wsm, S);
+        __syncthreads();
+        F::template middle<+1>(work, v, tid, Wsm, S);
+        if constexpr (HT) {
+            // g += wx_q . C2R(B_q): z[n] = (x[2n], x[2n+1]) at the last-stage positions
+            const float *wq = wxs + qi * S;
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (!ok[u]) continue;
-                const int idx = b0 + tid + u * G::NTH;
-                const int rr = idx / T, cc = idx - rr * T;
-                const float hx = outs[rr * XS + c2 + cc] * scale;
-                if (mode == FFT_PLAIN) {
-                    Fd.r[off[u]] = hx;
-                } else {
-                    const float d = hx - yv[u];
-                    if (mode == FFT_RESIDUAL) Fd.r[off[u]] = wv[u] * d;
-                    dsum += 0.5 * (double)wv[u] * (double)d * (double)d;
+            for (int i = 0; i < SL::BPT; ++i) {
+                int tt, j;
+                SL::bj(i, tid, tt, j);
+#pragma unroll
+                for (int r = 0; r < SL::R; ++r) {
+                    const float2 w = *reinterpret_cast<const float2 *>(wq + 2 * SL::out_n(j, r));
+                    float2 &o = acc[i * SL::R + r];
+                    o.x += w.x * v[i * SL::R + r].x;
+                    o.y += w.y * v[i * SL::R + r].y;
                 }
             }
         }
-        if (mode != FFT_PLAIN && A.partials) {
-            const double s = block_sum(dsum, red);
-            if (tid == 0) A.partials[blockIdx.x] = s;
-        }
-        return;
     }
-    // H^T: g = sum_q wx_q . C2R(B_q)
-    for (int idx = tid; idx < nrows * T; idx += G::NTH) gacc[idx] = 0.f;
-    const float2 *Bbase = base + (int64_t)S * LDF;
-    for (int q = t.q0; q <= t.q1; ++q) {
-        __syncthreads();
-        c2r_rows<S>(Bbase + ((int64_t)(q - t.q0) * T + r0) * LDF, nrows, work, outs, Wsm);
-        const float *wxq = A.wx + (size_t)q * A.Nx + Fd.ex0 + t.x0;
-        for (int idx = tid; idx < nrows * T; idx += G::NTH) {
-            const int rr = idx / T, cc = idx - rr * T;
-            const float wv = (t.x0 + cc < Fd.nx) ? __ldg(wxq + cc) : 0.f;
-            gacc[idx] += wv * (outs[rr * XS + cc] * scale);
+    // last-stage values -> outs (aliases work: middle() ended with a barrier)
+#pragma unroll
+    for (int i = 0; i < SL::BPT; ++i) {
+        int tt, j;
+        SL::bj(i, tid, tt, j);
+#pragma unroll
+        for (int r = 0; r < SL::R; ++r) {
+            float2 val;
+            if constexpr (HT) val = acc[i * SL::R + r];
+            else val = v[i * SL::R + r];
+            if (nq == 0) val = make_float2(0.f, 0.f);
+            *reinterpret_cast<float2 *>(outs + tt * XS + 2 * SL::out_n(j, r)) = val;
         }
     }
     __syncthreads();
-    for (int idx = tid; idx < nrows * T; idx += G::NTH) {
-        const int rr = idx / T, cc = idx - rr * T;
-        const int fy = t.y0 + r0 + rr, fx = t.x0 + cc;
-        if (fy < Fd.ny && fx < Fd.nx) Fd.g[(int64_t)fy * Fd.ep + fx] = gacc[idx];
+
+    if (ht) {
+        for (int idx = tid; idx < nrows * T; idx += G::NTH) {
+            const int rr = idx / T, cc = idx - rr * T;
+            const int fy = t.y0 + r0 + rr, fx = t.x0 + cc;
+            if (fy < Fd.ny && fx < Fd.nx) Fd.g[(int64_t)fy * Fd.ep + fx] = outs[rr * XS + cc] * scale;
+        }
+        return;
+    }
+    double dsum = 0.0;
+    constexpr int U = 8;
+    const int ntot = nrows * T;
+    for (int b0 = 0; b0 < ntot; b0 += U * G::NTH) {
+        float yv[U], wv[U];
+        int64_t off[U];
+        bool ok[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int idx = b0 + tid + u * G::NTH;
+            const int rr = idx / T, cc = idx - rr * T;
+            const int oi = t.y0 + r0 + rr, oj = t.x0 + cc;
+            ok[u] = idx < ntot && oi < Fd.my && oj < Fd.mx;
+            off[u] = (int64_t)oi * Fd.op + oj;
+            yv[u] = (ok[u] && mode != FFT_PLAIN) ? __ldg(Fd.y + off[u]) : 0.f;
+            wv[u] = (ok[u] && mode != FFT_PLAIN) ? (Fd.w ? __ldg(Fd.w + off[u]) : Fd.w_scalar) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (!ok[u]) continue;
+            const int idx = b0 + tid + u * G::NTH;
+            const int rr = idx / T, cc = idx - rr * T;
+            const float hx = outs[rr * XS + c2 + cc] * scale;
+            if (mode == FFT_PLAIN) {
+                Fd.r[off[u]] = hx;
+            } else {
+                const float d = hx - yv[u];
+                if (mode == FFT_RESIDUAL) Fd.r[off[u]] = wv[u] * d;
+                dsum += 0.5 * (double)wv[u] * (double)d * (double)d;
+            }
+        }
+    }
+    if (mode != FFT_PLAIN && A.partials) {
+        const double s = block_sum(dsum, red);
+        if (tid == 0) A.partials[blockIdx.x] = s;
     }
 }
 
@@ -784,9 +822,9 @@ static size_t smem_cols(int NP, int NQ) {
     return (size_t)S * 8 + (size_t)S * G::NB * 8 + 2 * (size_t)G::NB * G::CS * 8 + (size_t)NP * S * 4 + (size_t)NP * NQ * 4;
 }
 template <int S>
-static size_t smem_rows_inv(int T, bool ht = true) {
+static size_t smem_rows_inv(int NQ, bool ht = true) {
     using G = GR<S>;
-    return (size_t)S * 8 + (size_t)G::NB * G::RS * 8 + (size_t)G::NB * G::XS * 4 + (ht ? (size_t)G::NB * T * 4 : 0);
+    return (size_t)S * 8 + (size_t)G::NB * G::RS * 8 + (size_t)G::NB * C2R<S>::SS * 8 + (ht ? (size_t)NQ * S * 4 : 0);
 }
 
 template <int S>
@@ -794,7 +832,8 @@ static cudaError_t setup_attrs(int T, int NP, int NQ) {
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(k_rows_fwd<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rows_fwd<S>())) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(k_cols<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cols<S>(NP, NQ))) != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_rows_inv<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rows_inv<S>(T));
+    if ((e = cudaFuncSetAttribute(k_rows_inv<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rows_inv<S>(NQ, false))) != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_rows_inv<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rows_inv<S>(NQ));
 }
 
 template <int S>
@@ -816,7 +855,10 @@ template <int S>
 static cudaError_t run_rows_inv(const FftArgs &a, int ntiles, int T, int mode, cudaStream_t s) {
     if (ntiles == 0) return cudaSuccess;
     const int nblk = (T + GR<S>::NB - 1) / GR<S>::NB;
-    k_rows_inv<S><<<ntiles * nblk, GR<S>::NTH, smem_rows_inv<S>(T, mode == INV_HT), s>>>(a, mode);
+    if (mode == INV_HT)
+        k_rows_inv<S, true><<<ntiles * nblk, GR<S>::NTH, smem_rows_inv<S>(a.NQ, true), s>>>(a, mode);
+    else
+        k_rows_inv<S, false><<<ntiles * nblk, GR<S>::NTH, smem_rows_inv<S>(a.NQ, false), s>>>(a, mode);
     return cudaGetLastError();
 }
 
