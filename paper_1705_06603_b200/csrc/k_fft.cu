@@ -122,18 +122,22 @@ __host__ __device__ constexpr int fft_rad(int L, int s) {
 __host__ __device__ constexpr int fft_ns(int L, int s) { return s == 0 ? 1 : fft_ns(L, s - 1) * fft_rad(L, s - 1); }
 
 // One Stockham stage of NB batched length-L transforms at buf[t*STRIDE + n] executed
-// by NTH threads; butterfly b = tid + NTH*i maps to transform t = b % NB
-// (transform-fastest: a half-warp touches 16 transforms at one position, which
-// the padded STRIDE spreads over distinct banks) and butterfly j = b / NB.
+// by NTH threads.  Thread tid owns transform t = tid % NB (transform-fastest: a
+// quarter-/half-warp touches 8/16 transforms at one position, which the padded
+// STRIDE spreads over distinct banks) and the BPT consecutive butterflies
+// j = (tid / NB) * BPT + i.  Consecutive butterflies read and write adjacent
+// positions, so with an even STRIDE the exchanges move element pairs with 16-byte
+// shared-memory accesses (VEC): half the LDS/STS instructions of 8-byte accesses.
 template <int L, int NB, int STRIDE, int NTH, int s>
 struct Stage {
     static constexpr int R = fft_rad(L, s), Ns = fft_ns(L, s), LR = L / R;
     static constexpr int E = NB * L / NTH, BPT = E / R;
     static_assert(E % R == 0, "elements per thread must be a multiple of the radix");
+    static_assert(NTH * BPT * R == NB * L, "thread/butterfly mapping");
+    static constexpr bool VEC = (STRIDE % 2 == 0) && (BPT % 2 == 0) && (LR % 2 == 0);
     __device__ static __forceinline__ void bj(int i, int tid, int &t, int &j) {
-        const int b = tid + NTH * i;
-        t = b % NB;
-        j = b / NB;
+        t = tid % NB;
+        j = (tid / NB) * BPT + i;
     }
     __device__ static __forceinline__ int in_n(int j, int r) { return j + r * LR; }
     __device__ static __forceinline__ int out_n(int j, int r) { return (j / Ns) * Ns * R + (j % Ns) + r * Ns; }
@@ -170,22 +174,65 @@ struct Stage {
     }
     template <int SIGN>
     __device__ static __forceinline__ void load_bfly(const float2 *buf, float2 (&v)[E], int tid, const float2 *W, int S) {
+        if constexpr (VEC) {
+            // butterflies (i, i+1) read the adjacent positions (n, n+1)
 #pragma unroll
-        for (int i = 0; i < BPT; ++i) {
-            int t, j;
-            bj(i, tid, t, j);
+            for (int i = 0; i < BPT; i += 2) {
+                int t, j;
+                bj(i, tid, t, j);
 #pragma unroll
-            for (int r = 0; r < R; ++r) v[i * R + r] = buf[t * STRIDE + in_n(j, r)];
-            bfly<SIGN>(&v[i * R], j, W, S);
+                for (int r = 0; r < R; ++r) {
+                    const float4 q = *reinterpret_cast<const float4 *>(buf + t * STRIDE + in_n(j, r));
+                    v[i * R + r] = make_float2(q.x, q.y);
+                    v[(i + 1) * R + r] = make_float2(q.z, q.w);
+                }
+                bfly<SIGN>(&v[i * R], j, W, S);
+                bfly<SIGN>(&v[(i + 1) * R], j + 1, W, S);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < BPT; ++i) {
+                int t, j;
+                bj(i, tid, t, j);
+#pragma unroll
+                for (int r = 0; r < R; ++r) v[i * R + r] = buf[t * STRIDE + in_n(j, r)];
+                bfly<SIGN>(&v[i * R], j, W, S);
+            }
         }
     }
     __device__ static __forceinline__ void store(float2 *buf, const float2 (&v)[E], int tid) {
+        if constexpr (VEC && Ns == 1) {
+            // first stage: outputs r, r+1 of one butterfly are adjacent
 #pragma unroll
-        for (int i = 0; i < BPT; ++i) {
-            int t, j;
-            bj(i, tid, t, j);
+            for (int i = 0; i < BPT; ++i) {
+                int t, j;
+                bj(i, tid, t, j);
 #pragma unroll
-            for (int r = 0; r < R; ++r) buf[t * STRIDE + out_n(j, r)] = v[i * R + r];
+                for (int r = 0; r < R; r += 2) {
+                    const float2 a = v[i * R + r], b = v[i * R + r + 1];
+                    *reinterpret_cast<float4 *>(buf + t * STRIDE + out_n(j, r)) = make_float4(a.x, a.y, b.x, b.y);
+                }
+            }
+        } else if constexpr (VEC) {
+            // later stages: output r of butterflies j, j+1 (j even) are adjacent
+#pragma unroll
+            for (int i = 0; i < BPT; i += 2) {
+                int t, j;
+                bj(i, tid, t, j);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const float2 a = v[i * R + r], b = v[(i + 1) * R + r];
+                    *reinterpret_cast<float4 *>(buf + t * STRIDE + out_n(j, r)) = make_float4(a.x, a.y, b.x, b.y);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < BPT; ++i) {
+                int t, j;
+                bj(i, tid, t, j);
+#pragma unroll
+                for (int r = 0; r < R; ++r) buf[t * STRIDE + out_n(j, r)] = v[i * R + r];
+            }
         }
     }
 };
@@ -227,7 +274,7 @@ struct GR {
     static constexpr int SH = S / 2, NF = SH + 1;
     static constexpr int NTH = 256;
     static constexpr int NB = (S <= 64) ? 64 : (S <= 128) ? 32 : 16;
-    static constexpr int RS = SH + 1;    // smem row stride (float2): transform-fastest access is conflict-free
+    static constexpr int RS = SH + 2;    // smem row stride (float2): even (16-byte pair exchanges), conflict-free
     static constexpr int XS = S + 2;     // smem real-row stride (floats)
     using F = Fft<SH, NB, RS, NTH>;
     static constexpr int E = F::E;
@@ -352,21 +399,33 @@ __global__ void __launch_bounds__(256) k_rows_fwd(FftArgs A, int mode, int par, 
 }
 
 // ------------------------------------------------------------------ pass B / B'
-// Hhat chunk (S rows x NB columns starting at f0) -> smem hbuf[n][t] with cp.async
+// PSF spectra are stored with row pairs interleaved, in global memory
+// (element (n, f) at ((n >> 1) * LDF + f) * 2 + (n & 1)) and in the shared chunk
+// (element (n, t) at ((n >> 1) * NB + t) * 2 + (n & 1)): the values at rows n, n+1
+// of one column -- which the paired butterflies (j, j+1) of a thread need -- are
+// one 16-byte access, and a pair-row of a chunk is one contiguous 16*NB-byte run.
+__host__ __device__ __forceinline__ int64_t hg_idx(int n, int64_t f, int LDF) { return (((int64_t)(n >> 1) * LDF + f) << 1) + (n & 1); }
+template <int NB>
+__device__ __forceinline__ int hb_idx(int n, int t) { return (((n >> 1) * NB + t) << 1) + (n & 1); }
+
+// Hhat chunk (S rows x NB columns starting at f0) of spectrum Hk -> smem hbuf with cp.async
 template <int S, int NB, int NTH, int LDF>
-__device__ __forceinline__ void prefetch_hhat(float2 *hbuf, const float2 *Hk_f0, int tid) {
-    constexpr int V = NB / 2;                 // 16-byte vectors per row
-    constexpr int N = S * V;
+__device__ __forceinline__ void prefetch_hhat(float2 *hbuf, const float2 *Hk, int f0, int tid) {
+    constexpr int V = NB;                     // 16-byte vectors per pair-row
+    constexpr int N = (S / 2) * V;
 #pragma unroll
     for (int it = 0; it < (N + NTH - 1) / NTH; ++it) {
         const int idx = tid + it * NTH;
         if (idx < N) {
-            const int n = idx / V, v = idx % V;
-            __pipeline_memcpy_async(hbuf + n * NB + 2 * v, Hk_f0 + (int64_t)n * LDF + 2 * v, 16);
+            const int m = idx / V, v = idx % V;
+            __pipeline_memcpy_async(hbuf + m * 2 * NB + 2 * v, Hk + (((int64_t)m * LDF + f0) << 1) + 2 * v, 16);
         }
     }
     __pipeline_commit();
 }
+__device__ __forceinline__ float4 ld4(const float2 *p) { return *reinterpret_cast<const float4 *>(p); }
+__device__ __forceinline__ float2 lo2(float4 q) { return make_float2(q.x, q.y); }
+__device__ __forceinline__ float2 hi2(float4 q) { return make_float2(q.z, q.w); }
 
 // mode 0: H; 1: H^T; 2: PSF spectra (forward column DFT of hrows -> Hhat)
 template <int S>
@@ -404,13 +463,13 @@ __global__ void __launch_bounds__(GC<S>::NTH) k_cols(FftArgs A, int mode, const 
             S0::template bfly<-1>(&v[i * S0::R], j, Wsm, S);
         }
         F::template middle<-1>(work, v, tid, Wsm, S);
-        float2 *dst = hhat + (int64_t)tile * S * LDF + f0;
+        float2 *dst = hhat + (int64_t)tile * S * LDF;
 #pragma unroll
         for (int i = 0; i < SL::BPT; ++i) {
             int t, j;
             SL::bj(i, tid, t, j);
 #pragma unroll
-            for (int r = 0; r < SL::R; ++r) dst[(int64_t)SL::out_n(j, r) * LDF + t] = v[i * SL::R + r];
+            for (int r = 0; r < SL::R; ++r) dst[hg_idx(SL::out_n(j, r), f0 + t, LDF)] = v[i * SL::R + r];
         }
         return;
     }
@@ -433,9 +492,8 @@ __global__ void __launch_bounds__(GC<S>::NTH) k_cols(FftArgs A, int mode, const 
     }
     __syncthreads();
     const int nqt = td.q1 - td.q0 + 1;
-    auto hk = [&](int p, int q) {
-        return A.Hhat + (int64_t)slot_s[(p - td.p0) * nqt + (q - td.q0)] * S * LDF + f0;
-    };
+    auto hk = [&](int p, int q) { return A.Hhat + (int64_t)slot_s[(p - td.p0) * nqt + (q - td.q0)] * S * LDF; };
+    constexpr bool VP = S0::VEC && SL::VEC;        // paired 16-byte accesses
     const float *wys = wys_all;
     auto fill_wys = [&](int p) { wys = wys_all + (size_t)(p - td.p0) * S; };
 
@@ -462,33 +520,65 @@ __global__ void __launch_bounds__(GC<S>::NTH) k_cols(FftArgs A, int mode, const 
             }
             for (int p = td.p0; p <= td.p1; ++p) {
                 __syncthreads();
-                prefetch_hhat<S, NB, NTH, LDF>(hbuf, hk(p, q), tid);   // overlaps the FFT below
+                prefetch_hhat<S, NB, NTH, LDF>(hbuf, hk(p, q), f0, tid);   // overlaps the FFT below
                 fill_wys(p);
                 // stage 0 from colq, weighted by the row weight wy_p (constant along the row)
+                if constexpr (VP) {
 #pragma unroll
-                for (int i = 0; i < S0::BPT; ++i) {
-                    int t, j;
-                    S0::bj(i, tid, t, j);
+                    for (int i = 0; i < S0::BPT; i += 2) {
+                        int t, j;
+                        S0::bj(i, tid, t, j);
 #pragma unroll
-                    for (int r = 0; r < S0::R; ++r) {
-                        const int n = S0::in_n(j, r);
-                        const float2 c = colq[t * CS + n];
-                        const float wv = wys[n];
-                        v[i * S0::R + r] = make_float2(wv * c.x, wv * c.y);
+                        for (int r = 0; r < S0::R; ++r) {
+                            const int n = S0::in_n(j, r);
+                            const float4 c = ld4(colq + t * CS + n);
+                            const float2 wv = *reinterpret_cast<const float2 *>(wys + n);
+                            v[i * S0::R + r] = make_float2(wv.x * c.x, wv.x * c.y);
+                            v[(i + 1) * S0::R + r] = make_float2(wv.y * c.z, wv.y * c.w);
+                        }
+                        S0::template bfly<-1>(&v[i * S0::R], j, Wsm, S);
+                        S0::template bfly<-1>(&v[(i + 1) * S0::R], j + 1, Wsm, S);
                     }
-                    S0::template bfly<-1>(&v[i * S0::R], j, Wsm, S);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < S0::BPT; ++i) {
+                        int t, j;
+                        S0::bj(i, tid, t, j);
+#pragma unroll
+                        for (int r = 0; r < S0::R; ++r) {
+                            const int n = S0::in_n(j, r);
+                            const float2 c = colq[t * CS + n];
+                            const float wv = wys[n];
+                            v[i * S0::R + r] = make_float2(wv * c.x, wv * c.y);
+                        }
+                        S0::template bfly<-1>(&v[i * S0::R], j, Wsm, S);
+                    }
                 }
                 F::template middle<-1>(work, v, tid, Wsm, S);
                 __pipeline_wait_prior(0);
                 __syncthreads();
+                if constexpr (VP) {
 #pragma unroll
-                for (int i = 0; i < SL::BPT; ++i) {
-                    int t, j;
-                    SL::bj(i, tid, t, j);
+                    for (int i = 0; i < SL::BPT; i += 2) {
+                        int t, j;
+                        SL::bj(i, tid, t, j);
 #pragma unroll
-                    for (int r = 0; r < SL::R; ++r) {
-                        const float2 h = hbuf[SL::out_n(j, r) * NB + t];
-                        acc[i * SL::R + r] = cadd(acc[i * SL::R + r], cmul(v[i * SL::R + r], h));
+                        for (int r = 0; r < SL::R; ++r) {
+                            const float4 h = ld4(hbuf + hb_idx<NB>(SL::out_n(j, r), t));
+                            acc[i * SL::R + r] = cadd(acc[i * SL::R + r], cmul(v[i * SL::R + r], lo2(h)));
+                            acc[(i + 1) * SL::R + r] = cadd(acc[(i + 1) * SL::R + r], cmul(v[(i + 1) * SL::R + r], hi2(h)));
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < SL::BPT; ++i) {
+                        int t, j;
+                        SL::bj(i, tid, t, j);
+#pragma unroll
+                        for (int r = 0; r < SL::R; ++r) {
+                            const float2 h = hbuf[hb_idx<NB>(SL::out_n(j, r), t)];
+                            acc[i * SL::R + r] = cadd(acc[i * SL::R + r], cmul(v[i * SL::R + r], h));
+                        }
                     }
                 }
             }
@@ -517,7 +607,7 @@ __global__ void __launch_bounds__(GC<S>::NTH) k_cols(FftArgs A, int mode, const 
     }
 
     // mode 1 (H^T): R-hat = DFT_y of the r-window spectrum rows, kept in colq
-    if (td.p0 <= td.p1 && td.q0 <= td.q1) prefetch_hhat<S, NB, NTH, LDF>(hbuf, hk(td.p0, td.q0), tid);
+    if (td.p0 <= td.p1 && td.q0 <= td.q1) prefetch_hhat<S, NB, NTH, LDF>(hbuf, hk(td.p0, td.q0), f0, tid);
 #pragma unroll
     for (int i = 0; i < S0::BPT; ++i) {
         int t, j;
@@ -537,22 +627,39 @@ __global__ void __launch_bounds__(GC<S>::NTH) k_cols(FftArgs A, int mode, const 
             fill_wys(p);
             __pipeline_wait_prior(0);
             __syncthreads();
+            if constexpr (VP) {
 #pragma unroll
-            for (int i = 0; i < S0::BPT; ++i) {
-                int t, j;
-                S0::bj(i, tid, t, j);
+                for (int i = 0; i < S0::BPT; i += 2) {
+                    int t, j;
+                    S0::bj(i, tid, t, j);
 #pragma unroll
-                for (int r = 0; r < S0::R; ++r) {
-                    const int n = S0::in_n(j, r);
-                    v[i * S0::R + r] = cmulc(colq[t * CS + n], hbuf[n * NB + t]);
+                    for (int r = 0; r < S0::R; ++r) {
+                        const int n = S0::in_n(j, r);
+                        const float4 c = ld4(colq + t * CS + n), h = ld4(hbuf + hb_idx<NB>(n, t));
+                        v[i * S0::R + r] = cmulc(lo2(c), lo2(h));
+                        v[(i + 1) * S0::R + r] = cmulc(hi2(c), hi2(h));
+                    }
+                    S0::template bfly<+1>(&v[i * S0::R], j, Wsm, S);
+                    S0::template bfly<+1>(&v[(i + 1) * S0::R], j + 1, Wsm, S);
                 }
-                S0::template bfly<+1>(&v[i * S0::R], j, Wsm, S);
+            } else {
+#pragma unroll
+                for (int i = 0; i < S0::BPT; ++i) {
+                    int t, j;
+                    S0::bj(i, tid, t, j);
+#pragma unroll
+                    for (int r = 0; r < S0::R; ++r) {
+                        const int n = S0::in_n(j, r);
+                        v[i * S0::R + r] = cmulc(colq[t * CS + n], hbuf[hb_idx<NB>(n, t)]);
+                    }
+                    S0::template bfly<+1>(&v[i * S0::R], j, Wsm, S);
+                }
             }
             __syncthreads();      // hbuf consumed: prefetch the next PSF spectrum under the FFT
             {
                 int np = p + 1, nq = q;
                 if (np > td.p1) { np = td.p0; ++nq; }
-                if (nq <= td.q1) prefetch_hhat<S, NB, NTH, LDF>(hbuf, hk(np, nq), tid);
+                if (nq <= td.q1) prefetch_hhat<S, NB, NTH, LDF>(hbuf, hk(np, nq), f0, tid);
             }
             F::template middle<+1>(work, v, tid, Wsm, S);
 #pragma unroll
@@ -630,7 +737,7 @@ __global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
     using F = typename G::F;
     using SL = typename F::Last;
     constexpr int NB = G::NB, RS = G::RS, XS = G::XS, LDF = LD<S>::LDF, E = G::E;
-    static_assert(XS == 2 * RS, "outs aliases work");
+    static_assert(XS <= 2 * RS, "outs aliases work");
     extern __shared__ __align__(16) float2 sm2[];
     float2 *Wsm = sm2;
     float2 *work = Wsm + S;                                    // NB x RS; reused as outs (NB x XS reals)
