@@ -10,6 +10,8 @@
 //      this GPU, the received halo buffer otherwise.
 //  K6 k_tv_value / k_maxdiff (row a7): fp64 per-block partials of
 //      sum phi(D x) and max |x_f - x_f'| over shared pixels (A22).
+#include <cuda_pipeline.h>
+
 #include "epilogue.cuh"
 #include "kernels.hpp"
 
@@ -32,23 +34,16 @@ __global__ void __launch_bounds__(EPI_NT) k_update_from_g(const FacetDev *facets
     const float *__restrict__ x = F.x[par];
     const int tid = threadIdx.x;
     const bool interior = t.y0 >= 1 && t.y0 + UT_TY + 1 <= F.ny && t.x0 >= 4 && t.x0 + UT_TX + 4 <= F.nx;
+    // every load of the CTA is in flight before the first wait: the x halo streams into
+    // shared memory with 16-byte cp.async (interior tiles), g and u into registers
     if (interior) {
         constexpr int NV = XH / 4;                   // float4 per smem row
         for (int idx = tid; idx < (UT_TY + 2) * NV; idx += EPI_NT) {
             const int i = idx / NV, v = idx - i * NV;
-            const float4 val = __ldg(reinterpret_cast<const float4 *>(x + (int64_t)(t.y0 - 1 + i) * F.ep + t.x0 - 4) + v);
-            *reinterpret_cast<float4 *>(xh + i * XH + 4 * v) = val;
+            __pipeline_memcpy_async(xh + i * XH + 4 * v, x + (int64_t)(t.y0 - 1 + i) * F.ep + t.x0 - 4 + 4 * v, 16);
         }
-    } else {
-        for (int idx = tid; idx < (UT_TY + 2) * XH; idx += EPI_NT) {
-            const int i = idx / XH, c = idx - i * XH;
-            int fy = t.y0 - 1 + i, fx = t.x0 - 4 + c;
-            fy = ((fy % F.ny) + F.ny) % F.ny;
-            fx = ((fx % F.nx) + F.nx) % F.nx;
-            xh[idx] = x[(int64_t)fy * F.ep + fx];
-        }
+        __pipeline_commit();
     }
-    __syncthreads();
     const int tx = tid & 31, ty = tid >> 5;          // 32 strips of 4 columns x 8 row groups
     constexpr int KR = UT_TY / 8;
     const int lx0 = 4 * tx, fx0 = t.x0 + lx0;
@@ -57,7 +52,6 @@ __global__ void __launch_bounds__(EPI_NT) k_update_from_g(const FacetDev *facets
     float *__restrict__ up = F.u;
     float *__restrict__ vp = F.v;
     float *__restrict__ xo = F.x[par ^ 1];
-    // phase 1: every load of the strip in flight before any use
     float gv[KR][4], uv[KR][4];
 #pragma unroll
     for (int k = 0; k < KR; ++k) {
@@ -77,6 +71,18 @@ __global__ void __launch_bounds__(EPI_NT) k_update_from_g(const FacetDev *facets
             }
         }
     }
+    if (!interior) {
+        for (int idx = tid; idx < (UT_TY + 2) * XH; idx += EPI_NT) {
+            const int i = idx / XH, c = idx - i * XH;
+            int fy = t.y0 - 1 + i, fx = t.x0 - 4 + c;
+            fy = ((fy % F.ny) + F.ny) % F.ny;
+            fx = ((fx % F.nx) + F.nx) % F.nx;
+            xh[idx] = x[(int64_t)fy * F.ep + fx];
+        }
+    } else {
+        __pipeline_wait_prior(0);
+    }
+    __syncthreads();
     double rsum = 0.0;
 #pragma unroll
     for (int k = 0; k < KR; ++k) {
