@@ -41,19 +41,23 @@ def needs_build() -> bool:
     return any(os.path.getmtime(f) > t for f in sources() + headers())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> str:
+    """Build libdeblur.so; with `variant`, build libdeblur_<variant>.so from the same
+    sources with extra -D `defines` (A/B measurements via DEBLUR_LIB_VARIANT)."""
+    out = os.path.join(HERE, f"libdeblur_{variant}.so") if variant else OUT
+    bdir = os.path.join(BUILD, variant) if variant else BUILD
+    if not variant and not force and not needs_build():
         return OUT
     nd = nccl_dir()
-    os.makedirs(BUILD, exist_ok=True)
+    os.makedirs(bdir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
               "-I", os.path.join(nd, "include"), "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
     if os.environ.get("DEBLUR_PTXAS_V"):
         common += ["-Xptxas", "-v"]
 
     def compile_one(src):
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-        cmd = ["nvcc", *ARCH, *common, "-c", src, "-o", obj]
+        obj = os.path.join(bdir, os.path.basename(src) + ".o")
+        cmd = ["nvcc", *ARCH, *common, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -65,15 +69,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, sources()))
-    tmp = OUT + f".tmp{os.getpid()}"
+    tmp = out + f".tmp{os.getpid()}"
     cmd = ["nvcc", *ARCH, "-shared", "-o", tmp, *objs, "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
            "-Xlinker", "-rpath=" + os.path.join(nd, "lib"), "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--variant", default="")
+    ap.add_argument("-D", action="append", default=[], dest="defines")
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=True, variant=a.variant, defines=a.defines))

@@ -18,13 +18,16 @@
 namespace deblur {
 namespace {
 
+#ifndef K4_MINB
+#define K4_MINB 4
+#endif
 constexpr int UT_TY = 32, UT_TX = 128;   // update tile (matches the H^T tile grid)
 
 // K4: tile of UT_TY x UT_TX pixels; each thread owns a 4-pixel strip in 4 rows.
 // x halo staged with 16-byte loads (interior tiles) or a wrapped scalar path
 // (tiles touching the facet border: circular D within the facet, A2).
 template <int REG, bool NEU>
-__global__ void __launch_bounds__(EPI_NT) k_update_from_g(const FacetDev *facets, const TileDesc *tiles, int par,
+__global__ void __launch_bounds__(EPI_NT, K4_MINB) k_update_from_g(const FacetDev *facets, const TileDesc *tiles, int par,
                                                            int last, SolverConst sc, double *partials) {
     constexpr int XH = UT_TX + 8;                    // smem col c <-> facet col x0 - 4 + c
     __shared__ __align__(16) float xh[(UT_TY + 2) * XH];

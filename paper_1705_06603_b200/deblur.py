@@ -58,10 +58,12 @@ def lib():
     """Load libdeblur.so (building it in-tree if it is missing)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(_SO):
+        so = os.environ.get("DEBLUR_LIB_VARIANT")   # A/B measurement of an in-tree build variant
+        so = os.path.join(_HERE, so) if so else _SO
+        if not os.path.exists(so):
             from . import _build
             _build.build()
-        L = ctypes.CDLL(_SO)
+        L = ctypes.CDLL(so)
         h = ctypes.c_void_p
         sig = {
             "deblur_nccl_id": ([ctypes.c_void_p], ctypes.c_int),
