@@ -33,6 +33,7 @@ import numpy as np  # noqa: E402
 import synth  # noqa: E402
 
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC = os.path.join(ROOT, "profiles", "r1", "traffic.json")     # ncu --set full capture (tools/ncu_full.sh)
 NOMINAL_SMS = 148
 FMA_PER_SM_CLK = 128
 
@@ -183,6 +184,15 @@ def run_ours(args, rank, world, local):
 
     dom = max(kern, key=lambda k: kern[k][1])
     roofline = roof(dom)
+    # DRAM traffic of the same kernel from the committed `ncu --set full` capture (per launch)
+    try:
+        tr = json.load(open(TRAFFIC))
+        kt = tr["kernels"].get(dom)
+        if kt is not None and args.config == 4:
+            roofline["traffic"] = kt["bytes"]
+            roofline["traffic_source"] = os.path.relpath(TRAFFIC, ROOT) + " (" + tr["metric"] + ")"
+    except (OSError, ValueError, KeyError):
+        pass
     tot_ms_all = sum(x[1] for x in kern.values())
     breakdown = {}
     for k, v in kern.items():

@@ -144,6 +144,14 @@ DEBLUR_API deblur_status deblur_apply_HT_device(deblur_t h, const float *d_r, fl
  * v = 2x - u (a5), consensus and dual update (a6).  COLLECTIVE. */
 DEBLUR_API deblur_status deblur_iterate(deblur_t h, int32_t n);
 
+/* n iterations with the objective traced: trace[4k .. 4k+3] = deblur_objective at
+ * the state x^(k) before iteration k+1 (k = 0 .. n-1), i.e. the convergence
+ * history of Eq. (4) and of the consensus residual.  trace is a
+ * caller-allocated host array of 4n doubles.  Each entry costs one extra H
+ * evaluation (the objective's data term) and eager (non-graph) launches.
+ * COLLECTIVE; identical values on every rank. */
+DEBLUR_API deblur_status deblur_iterate_traced(deblur_t h, int32_t n, double *trace);
+
 /* out = {total, data, reg, consensus_maxdiff} at the current state (A22):
  * sum_f [1/2 sum_{O_f} w (H_f x_f - y)^2 + lambda sum_{P_f} phi(D x_f)] and
  * max |x_f(l) - x_g(l)| over shared pixels.  Identical on all ranks.  COLLECTIVE. */

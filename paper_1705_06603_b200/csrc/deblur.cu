@@ -746,6 +746,23 @@ deblur_status deblur_iterate(deblur_t h, int32_t n) {
     return finish(h);
 }
 
+deblur_status deblur_iterate_traced(deblur_t h, int32_t n, double *trace) {
+    deblur_status s = check_state(h);
+    if (s != DEBLUR_OK) return s;
+    if (n < 0) return h->fail(DEBLUR_EINVAL, "n must be >= 0");
+    if (!trace && n > 0) return h->fail(DEBLUR_EINVAL, "trace is NULL");
+    for (int32_t k = 0; k < n; ++k) {
+        double o[4];
+        if ((s = deblur_objective(h, o)) != DEBLUR_OK) return s;
+        trace[4 * k + 0] = o[0];
+        trace[4 * k + 1] = o[1];
+        trace[4 * k + 2] = o[2];
+        trace[4 * k + 3] = o[3];
+        if ((s = deblur_iterate(h, 1)) != DEBLUR_OK) return s;
+    }
+    return DEBLUR_OK;
+}
+
 deblur_status deblur_objective(deblur_t h, double out[4]) {
     deblur_status s = check_state(h);
     if (s != DEBLUR_OK) return s;

@@ -75,6 +75,7 @@ def lib():
             "deblur_apply_HT_device": ([h, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
             "deblur_iterate": ([h, ctypes.c_int32], ctypes.c_int),
             "deblur_objective": ([h, _dp], ctypes.c_int),
+            "deblur_iterate_traced": ([h, ctypes.c_int32, _dp], ctypes.c_int),
             "deblur_get_image": ([h, _fp], ctypes.c_int),
             "deblur_state_size": ([h, _lp], ctypes.c_int),
             "deblur_get_state": ([h, _fp, _fp], ctypes.c_int),
@@ -101,8 +102,8 @@ def lib():
 
 
 EXPORTED = ["deblur_nccl_id", "deblur_create", "deblur_destroy", "deblur_apply_H", "deblur_apply_HT",
-            "deblur_apply_H_device", "deblur_apply_HT_device", "deblur_iterate", "deblur_objective",
-            "deblur_get_image", "deblur_state_size", "deblur_get_state", "deblur_set_state", "deblur_reset",
+            "deblur_apply_H_device", "deblur_apply_HT_device", "deblur_iterate", "deblur_iterate_traced",
+            "deblur_objective", "deblur_get_image", "deblur_state_size", "deblur_get_state", "deblur_set_state", "deblur_reset",
             "deblur_get_step", "deblur_set_profiling", "deblur_kernel_stats", "deblur_kernel_name",
             "deblur_reset_stats", "deblur_kernel_work", "deblur_get_conv_path", "deblur_get_stream", "deblur_plan_facets", "deblur_plan_messages",
             "deblur_last_error"]
@@ -250,6 +251,12 @@ class Deblur:
     def iterate(self, n: int = 1):
         self._c(self._lib.deblur_iterate(self._h, int(n)))
         return self
+
+    def iterate_traced(self, n: int) -> np.ndarray:
+        """n iterations; row k = objective (total, data, reg, maxdiff) at x^(k)."""
+        out = np.zeros((max(int(n), 0), 4), np.float64)
+        self._c(self._lib.deblur_iterate_traced(self._h, int(n), out.ctypes.data_as(_dp)))
+        return out
 
     def objective(self):
         out = (ctypes.c_double * 4)()

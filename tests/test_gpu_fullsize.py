@@ -1,0 +1,138 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (AUTO path = FFT, CUDA-graph replay of deblur_iterate), on sampled outputs
+the fp64 oracle evaluates one by one.
+
+One full distributed iteration from a seeded state (set_state) is checked at
+sampled *single-owner* estimate pixels lying at least 2c+2 pixels inside their
+facet's estimate block.  There the Local-Solver step (Alg. 1, PAPER.md:226-229,
+rows a1-a4 of SURVEY §8a) and the single-owner dual update (Lemma 1 with one
+term, A8) depend only on a (4c+1)^2 neighbourhood of x and on u at the pixel:
+
+    r  = W (H x - y) on observed rows/cols [p - 2c, p]     (oracle H_window)
+    g  = (H^T r)(p)                                         (oracle HT_window)
+    t  = (D^T psi(D x))(p)                                  (oracle tv.grad on a crop)
+    x+ = max(0, x - tau (g + lambda t + gamma (x - u)))     (omega^F = 1)
+    u+ = u + rho (x+ - u)
+
+so the oracle recomputes x+ and u+ there exactly (fp64) without a full-size
+solve.  Band pixels are covered at reduced size by test_gpu_parity.py.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import Operator, geometry, solver, tv
+from paper_1705_06603_b200 import deblur as D
+
+pytestmark = pytest.mark.gpu
+
+IT_TOL = 1e-3            # BASELINE north_star: iterate within rel-L2 1e-3
+H_TOL = 1e-5
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _state(pb, facets, seed):
+    """x = max(0, edge-padded y) + small positive noise, u = x + noise: a state
+    near the data so that x+ is mostly unclipped and the prox term is active."""
+    rng = np.random.default_rng(seed)
+    c = (pb.P - 1) // 2
+    base = np.maximum(0.0, np.pad(pb.y, c, mode="edge")).astype(np.float32)
+    X = base + (0.002 * rng.random(base.shape, dtype=np.float32))
+    U = X + (0.002 * rng.standard_normal(base.shape, dtype=np.float32))
+    xs = np.concatenate([X[f.ey[0]:f.ey[1], f.ex[0]:f.ex[1]].ravel() for f in facets])
+    us = np.concatenate([U[f.ey[0]:f.ey[1], f.ex[0]:f.ex[1]].ravel() for f in facets])
+    return X, U, xs, us
+
+
+def _single_owner_samples(pb, facets, count, rng):
+    """(facet index, local row, local col) of single-owner pixels >= 2c+2 inside."""
+    c = (pb.P - 1) // 2
+    m = 2 * c + 2
+    out = []
+    while len(out) < count:
+        i = int(rng.integers(len(facets)))
+        f = facets[i]
+        ly = int(rng.integers(m, f.ey[1] - f.ey[0] - m))
+        lx = int(rng.integers(m, f.ex[1] - f.ex[0] - m))
+        gy, gx = f.ey[0] + ly, f.ex[0] + lx
+        n_own = sum(1 for g in facets if g.ey[0] <= gy < g.ey[1] and g.ex[0] <= gx < g.ex[1])
+        if n_own == 1:
+            out.append((i, ly, lx))
+    return out
+
+
+def _oracle_update(pb, op, X, U, tau, gy, gx):
+    """x+ and u+ at global estimate pixel (gy, gx) (single owner, interior)."""
+    c = op.c
+    xw = X[gy - 2 * c:gy + 2 * c + 1, gx - 2 * c:gx + 2 * c + 1].astype(np.float64)
+    hx = op.H_window(xw, gy - 2 * c, gx - 2 * c)                         # observed [p-2c, p]
+    yw = pb.y[gy - 2 * c:gy + 1, gx - 2 * c:gx + 1].astype(np.float64)
+    w = (pb.noise_w[gy - 2 * c:gy + 1, gx - 2 * c:gx + 1].astype(np.float64) if pb.noise_w is not None
+         else np.float64(np.float32(pb.noise_w_scalar)))
+    r = w * (hx - yw)
+    g = op.HT_window(r, gy - 2 * c, gx - 2 * c)[2 * c, 2 * c]
+    xc = X[gy - 2:gy + 3, gx - 2:gx + 3].astype(np.float64)
+    t = tv.grad(xc, pb.eps, pb.reg_kind, pb.tv_boundary)[2, 2]
+    x0 = float(X[gy, gx])
+    u0 = float(U[gy, gx])
+    xp = max(0.0, x0 - tau * (g + pb.lam * t + pb.gamma * (x0 - u0)))
+    return xp, u0 + pb.rho * (xp - u0)
+
+
+@pytest.mark.parametrize("k,count", [(4, 24), (5, 12)], ids=["c4", "c5"])
+def test_iterate_full_size_sampled(k, count):
+    pb = synth.make_config(k)
+    facets = geometry.plan(pb.ny, pb.nx, pb.P, pb.fy, pb.fx, pb.overlap)
+    w_max = float(pb.noise_w.max()) if pb.noise_w is not None else float(np.float32(pb.noise_w_scalar))
+    tau = solver.default_tau(pb.psfs, pb.wy, pb.wx, w_max, pb.lam, pb.eps, pb.reg_kind, pb.gamma)
+    X, U, xs, us = _state(pb, facets, seed=100 + k)
+    with D.Deblur.from_problem(pb, tau=tau) as dev:
+        assert dev.conv_path == D.CONV_FFT                       # the bench's AUTO choice at P >= 7
+        dev.set_state(xs, us)
+        dev.iterate(1)                                           # graph replay, as timed by bench.py
+        xg, ug = dev.get_state()
+    del xs, us
+    rng = np.random.default_rng(k)
+    samples = _single_owner_samples(pb, facets, count, rng)
+    offs = np.cumsum([0] + [(f.ey[1] - f.ey[0]) * (f.ex[1] - f.ex[0]) for f in facets])
+    op = Operator(pb.psfs, pb.wy, pb.wx)
+    got_x, got_u, ref_x, ref_u = [], [], [], []
+    for i, ly, lx in samples:
+        f = facets[i]
+        o = offs[i] + ly * (f.ex[1] - f.ex[0]) + lx
+        got_x.append(xg[o])
+        got_u.append(ug[o])
+        xp, up = _oracle_update(pb, op, X, U, tau, f.ey[0] + ly, f.ex[0] + lx)
+        ref_x.append(xp)
+        ref_u.append(up)
+    assert np.count_nonzero(ref_x) >= len(ref_x) // 2           # the step is not all clipped
+    assert rel_l2(got_x, ref_x) <= IT_TOL, rel_l2(got_x, ref_x)
+    assert rel_l2(got_u, ref_u) <= IT_TOL, rel_l2(got_u, ref_u)
+
+
+@pytest.mark.parametrize("count", [2000])
+def test_apply_c5_sampled(count):
+    """c5 (32768^2, 32x32 grid of 127x127 PSFs, 8x8 facets) H / H^T on one GPU,
+    sampled pixels including facet seams and image borders."""
+    pb = synth.make_config(5)
+    rng = np.random.default_rng(55)
+    x = (0.05 + rng.random((pb.ny, pb.nx), dtype=np.float32) * 0.5).astype(np.float32)
+    op = Operator(pb.psfs, pb.wy, pb.wx)
+    with D.Deblur.from_problem(pb) as dev:
+        hx = dev.apply_H(x)
+        oi, oj = rng.integers(0, pb.my, count), rng.integers(0, pb.mx, count)
+        oi[:6] = [0, pb.my - 1, 0, pb.my // 8, pb.my // 2, pb.my - 2]
+        ref = op.H_points(x, oi, oj)
+        assert rel_l2(hx[oi, oj], ref) <= H_TOL
+        del hx, x
+        r = rng.standard_normal((pb.my, pb.mx), dtype=np.float32)
+        g = dev.apply_HT(r)
+    ei, ej = rng.integers(0, pb.ny, count), rng.integers(0, pb.nx, count)
+    ei[:4] = [0, pb.ny - 1, 63, pb.ny - 64]
+    ref = op.HT_points(r, ei, ej)
+    assert rel_l2(g[ei, ej], ref) <= H_TOL

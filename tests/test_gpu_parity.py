@@ -260,3 +260,29 @@ def test_reset_default_init_and_image(path):
     np.testing.assert_array_equal(xs, xr.astype(np.float32))
     np.testing.assert_array_equal(us, ur.astype(np.float32))
     assert rel_l2(img, orc.image()) <= 1e-6
+
+
+@pytest.mark.parametrize("path", PATHS, ids=["direct", "fft"])
+def test_iterate_traced(path):
+    """deblur_iterate_traced: row k is the objective (Eq. (4), A22) at x^(k), equal
+    to the oracle's; the traced run leaves exactly the state of a plain run."""
+    pb = synth.make_config(2, n=300, facets=(2, 2), overlap=40)
+    orc = from_problem(pb)
+    ref = []
+    for _ in range(4):
+        ref.append(orc.objective())
+        orc.iterate(1)
+    with D.Deblur.from_problem(pb, conv_path=path, tau=orc.tau) as dev:
+        tr = dev.iterate_traced(4)
+        xs, us = dev.get_state()
+    with D.Deblur.from_problem(pb, conv_path=path, tau=orc.tau) as dev:
+        dev.iterate(4)
+        xp, up = dev.get_state()
+    np.testing.assert_array_equal(xs, xp)
+    np.testing.assert_array_equal(us, up)
+    xr, _ = orc.state()
+    for k in range(4):
+        for i in range(3):
+            assert abs(tr[k, i] - ref[k][i]) <= OBJ_TOL * abs(ref[k][i]) + 1e-12, (k, i, tr[k, i], ref[k][i])
+        assert abs(tr[k, 3] - ref[k][3]) <= IT_TOL * max(1.0, np.abs(xr).max())
+    assert tr[3, 0] < tr[0, 0]              # the objective decreases from the A6 start
