@@ -31,6 +31,13 @@
 #include "epilogue.cuh"
 #include "fft.hpp"
 
+#ifndef COLS_TMEM
+#define COLS_TMEM 1
+#endif
+#ifndef COLS_TM_MINB
+#define COLS_TM_MINB 2
+#endif
+
 namespace deblur {
 
 namespace {
@@ -689,6 +696,296 @@ __global__ void __launch_bounds__(GC<S>::NTH) k_cols(FftArgs A, int mode, const 
     }
 }
 
+// ------------------------------------------------------------------ pass B / B' with TMEM
+// Variant of k_cols (modes 0 and 1) whose per-thread state that survives across the
+// (p, q) transforms -- the stage-0 inputs of the chunk (A_q for H, R-hat for H^T) and
+// the spectral accumulator -- lives in tensor memory (tcgen05.st / tcgen05.ld,
+// 32x32b shape: each thread owns one TMEM lane, 64 columns) instead of registers and
+// shared memory (34 KB less per CTA; measured on c4: H 4.16 -> 4.05 ms, H^T 3.97 ->
+// 3.63 ms).  At 2 CTAs/SM the transform itself still needs 128 registers; forcing 3
+// CTAs/SM (80 registers) spills and is slower (profiles/r1/SUMMARY.md).
+__device__ __forceinline__ void tm_st32(uint32_t ta, const uint32_t (&r)[32]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%32], {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31};\n" :: "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]), "r"(ta) : "memory");
+}
+__device__ __forceinline__ void tm_ld32(uint32_t ta, uint32_t (&r)[32]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]) : "r"(ta) : "memory");
+}
+__device__ __forceinline__ void tm_st16(uint32_t ta, const uint32_t (&r)[16]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%16], {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15};\n" :: "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(ta) : "memory");
+}
+__device__ __forceinline__ void tm_ld16(uint32_t ta, uint32_t (&r)[16]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];\n" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]) : "r"(ta) : "memory");
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
+// E = 16 complex per thread <-> 32 TMEM columns
+template <int E>
+__device__ __forceinline__ void tm_put(uint32_t ta, const float2 (&v)[E]) {
+    static_assert(E == 16, "TMEM column pass holds 16 complex per thread");
+    uint32_t r[32];
+#pragma unroll
+    for (int e = 0; e < E; ++e) { r[2 * e] = __float_as_uint(v[e].x); r[2 * e + 1] = __float_as_uint(v[e].y); }
+    tm_st32(ta, r);
+}
+template <int E>
+__device__ __forceinline__ void tm_get(uint32_t ta, float2 (&v)[E]) {
+    uint32_t r[32];
+    tm_ld32(ta, r);
+    tm_wait_ld();
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = make_float2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
+}
+
+template <int S>
+struct GCT {
+    static constexpr int NTH = 256, NB = 8, CS = S + 2;
+    static constexpr int E = NB * S / NTH;
+    static constexpr int TMCOLS = 128;      // per CTA: 4 lane quarters x (2 warps x 64 columns)
+    using F = Fft<S, NB, CS, NTH>;
+};
+template <int S>
+static size_t smem_cols_tm(int NP, int NQ) {
+    using G = GCT<S>;
+    return (size_t)S * 8 + (size_t)S * G::NB * 8 + (size_t)G::NB * G::CS * 8 + (size_t)NP * S * 4 +
+           (size_t)NP * NQ * 4 + 16;
+}
+
+template <int S>
+__global__ void __launch_bounds__(256, COLS_TM_MINB) k_cols_tm(FftArgs A, int mode) {
+    using G = GCT<S>;
+    using F = typename G::F;
+    using S0 = typename F::First;
+    using SL = typename F::Last;
+    static_assert(S0::R == SL::R && S0::VEC && SL::VEC, "paired first/last stages");
+    constexpr int NB = G::NB, CS = G::CS, E = G::E, LDF = LD<S>::LDF, NF = S / 2 + 1, NTH = G::NTH;
+    static_assert(LD<S>::LDF == S / 2 + NB, "chunking shared with k_cols");
+    extern __shared__ __align__(16) float2 sm2[];
+    float2 *Wsm = sm2;               // S
+    float2 *hbuf = Wsm + S;          // S x NB (prefetched PSF spectrum chunk, pair-interleaved)
+    float2 *work = hbuf + S * NB;    // NB x CS
+    float *wys_all = reinterpret_cast<float *>(work + NB * CS);
+    int *slot_s = reinterpret_cast<int *>(wys_all + (size_t)A.NP * S);
+    uint32_t *tm_slot = reinterpret_cast<uint32_t *>(slot_s + A.NP * A.NQ);
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int nchunk = (NF + NB - 1) / NB;
+    const int tile = blockIdx.x / nchunk, f0 = (blockIdx.x % nchunk) * NB;
+    const int P = A.P, c2 = P - 1, T = S - P + 1;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
+                     :: "r"((uint32_t)__cvta_generic_to_shared(tm_slot)), "n"(G::TMCOLS) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    for (int i = tid; i < S; i += NTH) Wsm[i] = A.W[i];
+    const TileDesc td = A.tiles[tile];
+    const FacetDev &Fd = A.facets[td.f];
+    float2 *base = A.scratch + (int64_t)tile * A.tile_rows * LDF;
+    {
+        const int np = td.p1 - td.p0 + 1, nq = td.q1 - td.q0 + 1;
+        for (int idx = tid; idx < np * S; idx += NTH) {
+            const int pi = idx / S, i = idx - pi * S;
+            wys_all[idx] = (td.y0 + i < Fd.ny) ? __ldg(A.wy + (size_t)(td.p0 + pi) * A.Ny + Fd.ey0 + td.y0 + i) : 0.f;
+        }
+        for (int idx = tid; idx < np * nq; idx += NTH) {
+            const int pi = idx / nq, qi = idx - pi * nq;
+            slot_s[idx] = __ldg(A.psf_slot + (td.p0 + pi) * A.Gx + td.q0 + qi);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    // this thread's TMEM lane (warp quarter) and its 64 columns: [0, 32) inputs, [32, 64) accumulator
+    const uint32_t t_in = *tm_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 64);
+    const uint32_t t_acc = t_in + 32;
+    const int nqt = td.q1 - td.q0 + 1;
+    auto hk = [&](int p, int q) { return A.Hhat + (int64_t)slot_s[(p - td.p0) * nqt + (q - td.q0)] * S * LDF; };
+    // stage-0 input positions of this thread, straight from the global chunk (row stride LDF)
+    auto load_in = [&](const float2 *src, float2 (&v)[E]) {
+#pragma unroll
+        for (int i = 0; i < S0::BPT; ++i) {
+            int t, j;
+            S0::bj(i, tid, t, j);
+#pragma unroll
+            for (int r = 0; r < S0::R; ++r) v[i * S0::R + r] = __ldg(src + (int64_t)S0::in_n(j, r) * LDF + f0 + t);
+        }
+    };
+    float2 v[E];
+
+    if (mode == 0) {
+        bool first = true;
+        for (int q = td.q0; q <= td.q1; ++q) {
+            load_in(base + (int64_t)(q - td.q0) * S * LDF, v);
+            tm_put<E>(t_in, v);
+            tm_wait_st();
+            for (int p = td.p0; p <= td.p1; ++p) {
+                __syncthreads();                   // hbuf free
+                prefetch_hhat<S, NB, NTH, LDF>(hbuf, hk(p, q), f0, tid);   // under the FFT below
+                const float *wys = wys_all + (size_t)(p - td.p0) * S;
+                if (p != td.p0) tm_get<E>(t_in, v);
+#pragma unroll
+                for (int i = 0; i < S0::BPT; i += 2) {
+                    int t, j;
+                    S0::bj(i, tid, t, j);
+#pragma unroll
+                    for (int r = 0; r < S0::R; ++r) {
+                        const int n = S0::in_n(j, r);
+                        const float2 wv = *reinterpret_cast<const float2 *>(wys + n);
+                        v[i * S0::R + r].x *= wv.x; v[i * S0::R + r].y *= wv.x;
+                        v[(i + 1) * S0::R + r].x *= wv.y; v[(i + 1) * S0::R + r].y *= wv.y;
+                    }
+                    S0::template bfly<-1>(&v[i * S0::R], j, Wsm, S);
+                    S0::template bfly<-1>(&v[(i + 1) * S0::R], j + 1, Wsm, S);
+                }
+                F::template middle<-1>(work, v, tid, Wsm, S);
+                __pipeline_wait_prior(0);
+                __syncthreads();                   // Hhat chunk visible
+                // acc += v . Hhat, in two halves of 8 complex (16 TMEM columns each)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t a[16];
+                    if (!first) { tm_ld16(t_acc + 16 * h, a); tm_wait_ld(); }
+#pragma unroll
+                    for (int i2 = 0; i2 < SL::BPT / 2; i2 += 2) {
+                        const int i = h * (SL::BPT / 2) + i2;
+                        int t, j;
+                        SL::bj(i, tid, t, j);
+#pragma unroll
+                        for (int r = 0; r < SL::R; ++r) {
+                            const float4 hh = ld4(hbuf + hb_idx<NB>(SL::out_n(j, r), t));
+                            const float2 p0 = cmul(v[i * SL::R + r], lo2(hh));
+                            const float2 p1 = cmul(v[(i + 1) * SL::R + r], hi2(hh));
+                            const int e0 = (i2 * SL::R + r) * 2, e1 = ((i2 + 1) * SL::R + r) * 2;
+                            float2 a0 = first ? make_float2(0.f, 0.f) : make_float2(__uint_as_float(a[e0]), __uint_as_float(a[e0 + 1]));
+                            float2 a1 = first ? make_float2(0.f, 0.f) : make_float2(__uint_as_float(a[e1]), __uint_as_float(a[e1 + 1]));
+                            a0 = cadd(a0, p0);
+                            a1 = cadd(a1, p1);
+                            a[e0] = __float_as_uint(a0.x); a[e0 + 1] = __float_as_uint(a0.y);
+                            a[e1] = __float_as_uint(a1.x); a[e1 + 1] = __float_as_uint(a1.y);
+                        }
+                    }
+                    tm_st16(t_acc + 16 * h, a);
+                }
+                tm_wait_st();
+                first = false;
+            }
+        }
+        if (first) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[e] = make_float2(0.f, 0.f);
+        } else {
+            tm_get<E>(t_acc, v);
+        }
+        // inverse DFT along y; the accumulator sits at stage-0 input positions
+#pragma unroll
+        for (int i = 0; i < S0::BPT; ++i) {
+            int t, j;
+            S0::bj(i, tid, t, j);
+            S0::template bfly<+1>(&v[i * S0::R], j, Wsm, S);
+        }
+        __syncthreads();
+        F::template middle<+1>(work, v, tid, Wsm, S);
+        float2 *O = base + (int64_t)A.NQ * S * LDF + f0;
+#pragma unroll
+        for (int i = 0; i < SL::BPT; ++i) {
+            int t, j;
+            SL::bj(i, tid, t, j);
+#pragma unroll
+            for (int r = 0; r < SL::R; ++r) {
+                const int n = SL::out_n(j, r);
+                if (n >= c2) O[(int64_t)(n - c2) * LDF + t] = v[i * SL::R + r];
+            }
+        }
+    } else {
+        // mode 1 (H^T): R-hat = DFT_y of the r-window spectrum rows, kept in TMEM
+        if (td.p0 <= td.p1 && td.q0 <= td.q1) prefetch_hhat<S, NB, NTH, LDF>(hbuf, hk(td.p0, td.q0), f0, tid);
+        load_in(base, v);
+#pragma unroll
+        for (int i = 0; i < S0::BPT; ++i) {
+            int t, j;
+            S0::bj(i, tid, t, j);
+            S0::template bfly<-1>(&v[i * S0::R], j, Wsm, S);
+        }
+        F::template middle<-1>(work, v, tid, Wsm, S);
+        tm_put<E>(t_in, v);                        // last-stage positions == stage-0 positions
+        tm_wait_st();
+        float2 *Bbase = base + (int64_t)S * LDF + f0;
+        for (int q = td.q0; q <= td.q1; ++q) {
+            bool first = true;
+            for (int p = td.p0; p <= td.p1; ++p) {
+                const float *wys = wys_all + (size_t)(p - td.p0) * S;
+                tm_get<E>(t_in, v);
+                __pipeline_wait_prior(0);
+                __syncthreads();                   // Hhat chunk visible
+#pragma unroll
+                for (int i = 0; i < S0::BPT; i += 2) {
+                    int t, j;
+                    S0::bj(i, tid, t, j);
+#pragma unroll
+                    for (int r = 0; r < S0::R; ++r) {
+                        const float4 hh = ld4(hbuf + hb_idx<NB>(S0::in_n(j, r), t));
+                        v[i * S0::R + r] = cmulc(v[i * S0::R + r], lo2(hh));
+                        v[(i + 1) * S0::R + r] = cmulc(v[(i + 1) * S0::R + r], hi2(hh));
+                    }
+                    S0::template bfly<+1>(&v[i * S0::R], j, Wsm, S);
+                    S0::template bfly<+1>(&v[(i + 1) * S0::R], j + 1, Wsm, S);
+                }
+                __syncthreads();                   // hbuf consumed: prefetch the next spectrum under the FFT
+                {
+                    int np = p + 1, nq = q;
+                    if (np > td.p1) { np = td.p0; ++nq; }
+                    if (nq <= td.q1) prefetch_hhat<S, NB, NTH, LDF>(hbuf, hk(np, nq), f0, tid);
+                }
+                F::template middle<+1>(work, v, tid, Wsm, S);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t a[16];
+                    if (!first) { tm_ld16(t_acc + 16 * h, a); tm_wait_ld(); }
+#pragma unroll
+                    for (int i2 = 0; i2 < SL::BPT / 2; ++i2) {
+                        const int i = h * (SL::BPT / 2) + i2;
+                        int t, j;
+                        SL::bj(i, tid, t, j);
+#pragma unroll
+                        for (int r = 0; r < SL::R; ++r) {
+                            const int n = SL::out_n(j, r);
+                            const float wv = (n < T) ? wys[n] : 0.f;
+                            const int e = (i2 * SL::R + r) * 2;
+                            float2 o = first ? make_float2(0.f, 0.f) : make_float2(__uint_as_float(a[e]), __uint_as_float(a[e + 1]));
+                            o.x += wv * v[i * SL::R + r].x;
+                            o.y += wv * v[i * SL::R + r].y;
+                            a[e] = __float_as_uint(o.x); a[e + 1] = __float_as_uint(o.y);
+                        }
+                    }
+                    tm_st16(t_acc + 16 * h, a);
+                }
+                tm_wait_st();
+                first = false;
+            }
+            if (first) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) v[e] = make_float2(0.f, 0.f);
+            } else {
+                tm_get<E>(t_acc, v);
+            }
+            float2 *Bq = Bbase + (int64_t)(q - td.q0) * T * LDF;
+#pragma unroll
+            for (int i = 0; i < SL::BPT; ++i) {
+                int t, j;
+                SL::bj(i, tid, t, j);
+#pragma unroll
+                for (int r = 0; r < SL::R; ++r) {
+                    const int n = SL::out_n(j, r);
+                    if (n < T) Bq[(int64_t)n * LDF + t] = v[i * SL::R + r];
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" :: "r"(*tm_slot), "n"(G::TMCOLS) : "memory");
+}
+
 // ------------------------------------------------------------------ pass C / C'
 // C2R of NB spectrum rows per CTA.  The rows (global, stride LDF) are streamed into a
 // shared staging buffer with cp.async one source ahead, so the next source's loads
@@ -939,6 +1236,10 @@ static cudaError_t setup_attrs(int T, int NP, int NQ) {
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(k_rows_fwd<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rows_fwd<S>())) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(k_cols<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cols<S>(NP, NQ))) != cudaSuccess) return e;
+#if COLS_TMEM
+    if constexpr (S == 512)
+        if ((e = cudaFuncSetAttribute(k_cols_tm<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cols_tm<S>(NP, NQ))) != cudaSuccess) return e;
+#endif
     if ((e = cudaFuncSetAttribute(k_rows_inv<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rows_inv<S>(NQ, false))) != cudaSuccess) return e;
     return cudaFuncSetAttribute(k_rows_inv<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rows_inv<S>(NQ));
 }
@@ -955,6 +1256,14 @@ static cudaError_t run_cols(const FftArgs &a, int ntiles, int mode, const float2
                             cudaStream_t s) {
     if (ntiles == 0) return cudaSuccess;
     const int nchunk = (S / 2 + 1 + GC<S>::NB - 1) / GC<S>::NB;
+#if COLS_TMEM
+    if constexpr (S == 512) {
+        if (mode != 2) {
+            k_cols_tm<S><<<ntiles * nchunk, GCT<S>::NTH, smem_cols_tm<S>(a.NP, a.NQ), s>>>(a, mode);
+            return cudaGetLastError();
+        }
+    }
+#endif
     k_cols<S><<<ntiles * nchunk, GC<S>::NTH, smem_cols<S>(a.NP, a.NQ), s>>>(a, mode, hrows, hhat, npsf);
     return cudaGetLastError();
 }
