@@ -65,7 +65,7 @@ extern "C" {
 #define DEBLUR_API
 #endif
 
-#define DEBLUR_ABI_VERSION 1
+#define DEBLUR_ABI_VERSION 2
 
 typedef struct deblur_ctx *deblur_t;
 
@@ -79,6 +79,25 @@ typedef enum {
     DEBLUR_ENUMERIC = -6, /* non-finite objective partial (names facet) */
     DEBLUR_ESTATE = -7    /* handle poisoned, or call not valid in this state */
 } deblur_status;
+
+/* Facet-local operator model.
+ *   DEBLUR_OP_INTERP: H_f = the global PSF-interpolation operator H
+ *     restricted to the facet's observed rows O_f and estimate columns P_f (R1);
+ *     consensus weights omega^F = the A13 ramps on the shared bands.
+ *   DEBLUR_OP_PER_NODE: the paper's node model: facet
+ *     (a, b) of an F_y x F_x grid with F = G owns PSF k = a*G_x + b and its local
+ *     operator is the valid convolution with that single PSF, H_f = C_f calH_f (no
+ *     interpolation weights inside H_f); alpha_f = gamma * omega_f with omega_f =
+ *     interp_wy[a] (x) interp_wx[b] (the interpolation weights of its PSF), so the
+ *     consensus z = sum_f omega_f v_f / sum_f omega_f and the prox term
+ *     gamma omega_f (x - u) act with the interpolation weights; get_image returns
+ *     sum_f omega_f x_f / sum_f omega_f.  Requires psf_gy == facet_gy,
+ *     psf_gx == facet_gx and sum_{f containing l} omega_f(l) > 0 at every
+ *     estimate pixel (else DEBLUR_EINVAL naming the axis and pixel). */
+typedef enum {
+    DEBLUR_OP_INTERP = 0,
+    DEBLUR_OP_PER_NODE = 1
+} deblur_operator_mode;
 
 /* Blur-operator implementation for H / H^T (a1, a2 of §8a). */
 typedef enum {
@@ -118,6 +137,7 @@ typedef struct {
     int32_t conv_path;            /* deblur_conv_path */
     int32_t rank, world, device;  /* SPMD rank / world size; CUDA device ordinal */
     const void *nccl_id;          /* 128-byte ncclUniqueId identical on all ranks; NULL if world == 1 */
+    int32_t operator_mode;        /* deblur_operator_mode (default DEBLUR_OP_INTERP) */
 } deblur_params;
 
 /* 128-byte NCCL unique id for a world > 1 run: call on rank 0, broadcast

@@ -15,6 +15,14 @@ with the readings of SURVEY §8c:
   A8/A9  consensus divides by the computed sum of weights, facets in ascending id
   A20    every facet uses its full W_i (no multiplicity division)
   A22    objective = sum_f [data_f + lambda reg_f] at the current x (+ max |x_i - x_j|)
+Operator modes (NEXT-2):
+  0  H_i = the global PSF-interpolation H (PAPER.md:107) restricted to facet i (R1);
+     omega_i = the A13 ramps (partition of unity on every band)
+  1  per-node: facet (a, b) holds PSF h_i, i = a G_x + b,
+     and H_i = C_i calH_i is the valid convolution with h_i alone; omega_i = the
+     interpolation weights wy[a] (x) wx[b] of that PSF on the facet's estimate block;
+     the image is sum_i omega_i x_i / sum_i omega_i (the weights need not sum to 1
+     on a facet union)
 """
 from __future__ import annotations
 
@@ -88,16 +96,29 @@ class Deblur:
     """Oracle state for one problem: per-facet x_f, u_f (fp64)."""
 
     def __init__(self, psfs, wy, wx, y, w, Fy: int, Fx: int, overlap: int, params: Params,
-                 tau: Optional[float] = None, x0: Optional[np.ndarray] = None):
+                 tau: Optional[float] = None, x0: Optional[np.ndarray] = None, operator_mode: int = 0):
         self.op = Operator(psfs, wy, wx)
         self.prm = params
+        self.operator_mode = int(operator_mode)
         self.y = np.asarray(y, np.float64)
         self.w = np.broadcast_to(np.asarray(w, np.float64), self.y.shape)
         assert self.y.shape == (self.op.My, self.op.Mx)
         self.facets = geometry.plan(self.op.Ny, self.op.Nx, self.op.P, Fy, Fx, overlap)
         self.windows = [(slice(*f.ey), slice(*f.ex)) for f in self.facets]
         self.owin = [(slice(*f.oy), slice(*f.ox)) for f in self.facets]
-        self.omegas = [f.omega() for f in self.facets]
+        if self.operator_mode == 0:
+            self.omegas = [f.omega() for f in self.facets]
+            self.ops = [self.op] * len(self.facets)
+        else:
+            # per-node: facet grid = PSF grid; facet (a, b) blurs with PSF a*G_x + b only
+            assert (Fy, Fx) == (self.op.gy, self.op.gx), "per-node mode needs facet grid == PSF grid"
+            wy64 = np.asarray(wy, np.float64)
+            wx64 = np.asarray(wx, np.float64)
+            self.omegas = [np.outer(wy64[f.fy, f.ey[0]:f.ey[1]], wx64[f.fx, f.ex[0]:f.ex[1]]) for f in self.facets]
+            ones_y = np.ones((1, self.op.Ny))
+            ones_x = np.ones((1, self.op.Nx))
+            self.ops = [Operator(np.asarray(psfs)[f.fy * self.op.gx + f.fx][None], ones_y, ones_x)
+                        for f in self.facets]
         self.tau = default_tau(psfs, wy, wx, float(self.w.max()), params.lam, params.eps,
                                params.reg_kind, params.gamma) if tau is None else float(tau)
         if x0 is None:                                   # A6
@@ -115,7 +136,7 @@ class Deblur:
     def residual(self, i: int, xi: np.ndarray) -> np.ndarray:
         """r = W_i (H_i x_i - y_i) on O_i."""
         f = self.facets[i]
-        hx = self.op.H_window(xi, f.ey[0], f.ex[0])
+        hx = self.ops[i].H_window(xi, f.ey[0], f.ex[0])
         return self.w[self.owin[i]] * (hx - self.y[self.owin[i]])
 
     def local_grad(self, i: int, xi: np.ndarray, ui: np.ndarray) -> np.ndarray:
@@ -123,7 +144,7 @@ class Deblur:
         f = self.facets[i]
         p = self.prm
         r = self.residual(i, xi)
-        g = self.op.HT_window(r, f.ey[0], f.ex[0])
+        g = self.ops[i].HT_window(r, f.ey[0], f.ex[0])
         g = g + p.lam * tv.grad(xi, p.eps, p.reg_kind, p.tv_boundary)
         g = g + p.gamma * self.omegas[i] * (xi - ui)
         return g
@@ -148,7 +169,7 @@ class Deblur:
         data = 0.0
         reg = 0.0
         for i, f in enumerate(self.facets):
-            hx = self.op.H_window(self.x[i], f.ey[0], f.ex[0])
+            hx = self.ops[i].H_window(self.x[i], f.ey[0], f.ex[0])
             d = hx - self.y[self.owin[i]]
             data += 0.5 * float((self.w[self.owin[i]] * d * d).sum())
             reg += p.lam * tv.value(self.x[i], p.eps, p.reg_kind, p.tv_boundary)
@@ -166,9 +187,11 @@ class Deblur:
     def image(self) -> np.ndarray:
         """x_hat = sum_f omega^F_f x_f (A7)."""
         out = np.zeros(self.shape)
+        den = np.zeros(self.shape)
         for win, om, xi in zip(self.windows, self.omegas, self.x):
             out[win] += om * xi
-        return out
+            den[win] += om
+        return out if self.operator_mode == 0 else out / den
 
     def state(self):
         """Concatenated facets in planner (ascending id) order: (x, u)."""
@@ -182,4 +205,5 @@ def from_problem(pb, tau: Optional[float] = None, **over) -> Deblur:
     for k, v in over.items():
         setattr(prm, k, v)
     w = pb.noise_w if pb.noise_w is not None else np.float64(np.float32(pb.noise_w_scalar))
-    return Deblur(pb.psfs, pb.wy, pb.wx, pb.y, w, pb.fy, pb.fx, pb.overlap, prm, tau=tau, x0=pb.x0)
+    return Deblur(pb.psfs, pb.wy, pb.wx, pb.y, w, pb.fy, pb.fx, pb.overlap, prm, tau=tau, x0=pb.x0,
+                  operator_mode=getattr(pb, "operator_mode", 0))

@@ -62,6 +62,11 @@ struct deblur_ctx {
     FacetDev *d_facets_alt = nullptr;     // x[] -> g (apply_H input)
     std::vector<void *> allocs;
     float *d_psfs = nullptr, *d_wy = nullptr, *d_wx = nullptr;
+    // weights the operator kernels apply inside H_f: the interpolation weights (mode
+    // INTERP) or all-ones rows with one PSF per facet (mode PER_NODE)
+    float *d_owy = nullptr, *d_owx = nullptr;
+    bool per_node = false;
+    float *d_wsum = nullptr;          // per-node get_image normalisation
     std::vector<TileDesc> tilesH, tilesHT;
     TileDesc *d_tilesH = nullptr, *d_tilesHT = nullptr;
     std::vector<BandRect> rects;
@@ -150,7 +155,7 @@ struct deblur_ctx {
         a.facets = facets;
         a.tiles = ht ? d_tilesHT : d_tilesH;
         a.ntiles = (int)(ht ? tilesHT.size() : tilesH.size());
-        a.psfs = d_psfs; a.wy = d_wy; a.wx = d_wx;
+        a.psfs = d_psfs; a.wy = d_owy; a.wx = d_owx;
         a.P = plan.P; a.Gx = prm.psf_gx; a.Ny = (int)plan.ny; a.Nx = (int)plan.nx;
         a.partials = d_partials;
         return a;
@@ -195,7 +200,47 @@ deblur_status validate(const deblur_params *p, std::string &err) {
     if (p->world < 1 || p->rank < 0 || p->rank >= p->world) { err = "rank/world out of range"; return DEBLUR_EINVAL; }
     if (p->world > 1 && !p->nccl_id) { err = "nccl_id is NULL with world > 1"; return DEBLUR_EINVAL; }
     if (!(std::isfinite(p->tau))) { err = "tau must be finite"; return DEBLUR_EINVAL; }
+    if (p->operator_mode != DEBLUR_OP_INTERP && p->operator_mode != DEBLUR_OP_PER_NODE) {
+        err = "operator_mode must be 0 (interpolated H) or 1 (per-node PSFs)";
+        return DEBLUR_EINVAL;
+    }
+    if (p->operator_mode == DEBLUR_OP_PER_NODE && (p->psf_gy != p->facet_gy || p->psf_gx != p->facet_gx)) {
+        o << "per-node operator mode needs the facet grid to equal the PSF grid (facets " << p->facet_gy << "x"
+          << p->facet_gx << ", PSFs " << p->psf_gy << "x" << p->psf_gx << ")";
+        err = o.str();
+        return DEBLUR_EINVAL;
+    }
     return DEBLUR_OK;
+}
+
+// Per-node mode: every estimate pixel needs a positive consensus weight sum over the
+// facets containing it (P:201 divides by it).  Separable: checked per axis.
+static std::string check_node_weights(const Plan &pl, const float *wy, const float *wx) {
+    for (int axis = 0; axis < 2; ++axis) {
+        const int F = axis == 0 ? pl.Fy : pl.Fx;
+        const int64_t n = axis == 0 ? pl.ny : pl.nx;
+        const std::vector<AxisFacet> &af = axis == 0 ? pl.ay : pl.ax;
+        const float *w = axis == 0 ? wy : wx;
+        std::vector<double> sum(n, 0.0);
+        for (int k = 0; k < F; ++k)
+            for (int64_t i = af[k].e_lo; i < af[k].e_hi; ++i) {
+                const double v = w[(int64_t)k * n + i];
+                if (!(v >= 0.0)) {
+                    std::ostringstream o;
+                    o << (axis == 0 ? "interp_wy" : "interp_wx") << "[" << k << "][" << i << "] is negative or NaN";
+                    return o.str();
+                }
+                sum[i] += v;
+            }
+        for (int64_t i = 0; i < n; ++i)
+            if (!(sum[i] > 0.0)) {
+                std::ostringstream o;
+                o << "per-node mode: the consensus weights of the facets containing " << (axis == 0 ? "row " : "column ")
+                  << i << " sum to 0";
+                return o.str();
+            }
+    }
+    return "";
 }
 
 // A4': tau = 1/L, L = max(w) S^2 a_row a_col + lambda * 8 * Lip(psi) + gamma
@@ -482,6 +527,11 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
     if (!err.empty()) { g_last_error = err; return DEBLUR_ESHAPE; }
     const Plan &pl = h->plan;
     const int P = pl.P;
+    h->per_node = p->operator_mode == DEBLUR_OP_PER_NODE;
+    if (h->per_node) {
+        err = check_node_weights(pl, p->interp_wy, p->interp_wx);
+        if (!err.empty()) { g_last_error = err; return DEBLUR_EINVAL; }
+    }
 
     // device
     int ndev = 0;
@@ -526,19 +576,32 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
     CUC(cudaMemcpy(h->d_wx, p->interp_wx, sizeof(float) * p->psf_gx * p->nx, cudaMemcpyHostToDevice));
     h->h_wy.assign(p->interp_wy, p->interp_wy + (size_t)p->psf_gy * p->ny);
     h->h_wx.assign(p->interp_wx, p->interp_wx + (size_t)p->psf_gx * p->nx);
+    h->d_owy = h->d_wy;
+    h->d_owx = h->d_wx;
+    if (h->per_node) {
+        const std::vector<float> oy((size_t)p->psf_gy * p->ny, 1.f), ox((size_t)p->psf_gx * p->nx, 1.f);
+        CUC(h->dalloc(&h->d_owy, oy.size()));
+        CUC(h->dalloc(&h->d_owx, ox.size()));
+        CUC(cudaMemcpy(h->d_owy, oy.data(), sizeof(float) * oy.size(), cudaMemcpyHostToDevice));
+        CUC(cudaMemcpy(h->d_owx, ox.data(), sizeof(float) * ox.size(), cudaMemcpyHostToDevice));
+    }
 
     // local facets
     h->local_index.assign(pl.facets.size(), -1);
     for (const auto &f : pl.facets)
         if (f.owner == h->rank) { h->local_index[f.id] = (int)h->local.size(); h->local.push_back(f.id); }
-    auto axisw = [](int64_t e0, int64_t e1, int64_t pe, int64_t ns) {
+    auto axisw = [](int64_t e0, int64_t e1, int64_t pe, int64_t ns, const float *w) {
         AxisW a;
         a.e0 = (int)e0; a.n = (int)(e1 - e0);
         a.b_prev = (int)(pe - e0); a.b_next = (int)(ns - e0);
         a.s_prev = (int)e0; a.e_prev = (int)pe;
         a.s_next = (int)ns; a.e_next = (int)e1;
+        a.w = w;
         return a;
     };
+    // per-node consensus weights: facet (a, b) uses interp_wy[a], interp_wx[b]
+    auto node_wy = [&](const FacetPlan &f) { return h->per_node ? h->d_wy + (size_t)f.fy * p->ny : nullptr; };
+    auto node_wx = [&](const FacetPlan &f) { return h->per_node ? h->d_wx + (size_t)f.fx * p->nx : nullptr; };
     for (int id : h->local) {
         const FacetPlan &fp = pl.facets[id];
         FacetDev F{};
@@ -561,8 +624,8 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
                                   cudaMemcpyHostToDevice, h->stream));
         }
         F.y = y_; F.w = w_; F.w_scalar = p->noise_w_scalar;
-        F.ay = axisw(fp.ey0, fp.ey1, fp.py_e, fp.ny_s);
-        F.ax = axisw(fp.ex0, fp.ex1, fp.px_e, fp.nx_s);
+        F.ay = axisw(fp.ey0, fp.ey1, fp.py_e, fp.ny_s, node_wy(fp));
+        F.ax = axisw(fp.ex0, fp.ex1, fp.px_e, fp.nx_s, node_wx(fp));
         for (int dy = 0; dy < 3; ++dy)
             for (int dx = 0; dx < 3; ++dx) F.nb[dy][dx].id = -1;
         h->fh.push_back(F);
@@ -589,8 +652,8 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
                 const FacetPlan &np = pl.facets[gy * pl.Fx + gx];
                 Neighbour &nb = F.nb[dy + 1][dx + 1];
                 nb.id = np.id;
-                nb.ay = axisw(np.ey0, np.ey1, np.py_e, np.ny_s);
-                nb.ax = axisw(np.ex0, np.ex1, np.px_e, np.nx_s);
+                nb.ay = axisw(np.ey0, np.ey1, np.py_e, np.ny_s, node_wy(np));
+                nb.ax = axisw(np.ex0, np.ex1, np.px_e, np.nx_s, node_wx(np));
                 const int nli = h->local_index[np.id];
                 if (nli >= 0) {
                     const FacetDev &N = (nli == (int)li) ? F : h->fh[nli];
@@ -625,6 +688,10 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
     nzy.build(p->interp_wy, p->psf_gy, p->ny);
     nzx.build(p->interp_wx, p->psf_gx, p->nx);
     const int tyH = direct_ty_H(P), tyHT = direct_ty_HT(P), TXd = DIRECT_TX;
+    auto node_range = [](TileDesc &t, const FacetPlan &f) {   // the facet's own PSF only
+        t.p0 = t.p1 = f.fy;
+        t.q0 = t.q1 = f.fx;
+    };
     for (size_t li = 0; li < h->local.size(); ++li) {
         const FacetDev &F = h->fh[li];
         for (int y0 = 0; y0 < F.my; y0 += tyH)
@@ -632,6 +699,7 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
                 TileDesc t{(int)li, y0, x0, 0, -1, 0, -1};
                 nzy.range(F.ey0 + y0, F.ey0 + std::min(y0 + tyH + P - 1, F.ny), t.p0, t.p1);
                 nzx.range(F.ex0 + x0, F.ex0 + std::min(x0 + TXd + P - 1, F.nx), t.q0, t.q1);
+                if (h->per_node) node_range(t, pl.facets[F.id]);
                 h->tilesH.push_back(t);
             }
         for (int y0 = 0; y0 < F.ny; y0 += tyHT)
@@ -639,6 +707,7 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
                 TileDesc t{(int)li, y0, x0, 0, -1, 0, -1};
                 nzy.range(F.ey0 + y0, F.ey0 + std::min(y0 + tyHT, F.ny), t.p0, t.p1);
                 nzx.range(F.ex0 + x0, F.ex0 + std::min(x0 + TXd, F.nx), t.q0, t.q1);
+                if (h->per_node) node_range(t, pl.facets[F.id]);
                 h->tilesHT.push_back(t);
             }
     }
@@ -675,8 +744,8 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
     // FFT path plan
     if (h->conv_path == DEBLUR_CONV_FFT) {
         std::string ferr;
-        h->fft = fft_create(pl, h->local, h->fh, h->d_psfs, h->d_wy, h->d_wx, p->psf_gy, p->psf_gx, h->h_wy.data(),
-                            h->h_wx.data(), h->stream, ferr);
+        h->fft = fft_create(pl, h->local, h->fh, h->d_psfs, h->d_owy, h->d_owx, p->psf_gy, p->psf_gx, h->h_wy.data(),
+                            h->h_wx.data(), h->per_node, h->stream, ferr);
         if (!h->fft) { g_last_error = "FFT path: " + ferr; return DEBLUR_ECUDA; }
     }
 
@@ -1042,7 +1111,14 @@ deblur_status deblur_get_image(deblur_t h, float *x) {
         if (!h->d_image) CU(h->dalloc(&h->d_image, (size_t)pl.ny * pl.nx));
         float *img = h->d_image;
         CU(cudaMemsetAsync(img, 0, (size_t)pl.ny * pl.nx * 4, h->stream));
-        for (size_t li = 0; li < h->local.size(); ++li) CU(launch_blend(h->fh[li], h->par, img, pl.nx, h->stream));
+        float *wsum = nullptr;
+        if (h->per_node) {      // per-node weights need not sum to 1 on every facet union
+            if (!h->d_wsum) CU(h->dalloc(&h->d_wsum, (size_t)pl.ny * pl.nx));
+            wsum = h->d_wsum;
+            CU(cudaMemsetAsync(wsum, 0, (size_t)pl.ny * pl.nx * 4, h->stream));
+        }
+        for (size_t li = 0; li < h->local.size(); ++li) CU(launch_blend(h->fh[li], h->par, img, wsum, pl.nx, h->stream));
+        if (wsum) CU(launch_normalize(img, wsum, (int64_t)pl.ny * pl.nx, h->stream));
         CU(cudaMemcpyAsync(x, img, (size_t)pl.ny * pl.nx * 4, cudaMemcpyDeviceToHost, h->stream));
         return finish(h);
     }
@@ -1066,18 +1142,28 @@ deblur_status deblur_get_image(deblur_t h, float *x) {
     }
     if (h->rank != 0) return DEBLUR_OK;
     std::fill(x, x + pl.ny * pl.nx, 0.f);
+    std::vector<float> wsum(h->per_node ? (size_t)pl.ny * pl.nx : 0, 0.f);
     for (const auto &fp : pl.facets) {
+        // host copies of the device AxisW (per-node: host weight rows)
         const AxisW ay = {(int)fp.ey0, (int)(fp.ey1 - fp.ey0), (int)(fp.py_e - fp.ey0), (int)(fp.ny_s - fp.ey0),
-                          (int)fp.ey0, (int)fp.py_e, (int)fp.ny_s, (int)fp.ey1};
+                          (int)fp.ey0, (int)fp.py_e, (int)fp.ny_s, (int)fp.ey1,
+                          h->per_node ? h->h_wy.data() + (size_t)fp.fy * pl.ny : nullptr};
         const AxisW ax = {(int)fp.ex0, (int)(fp.ex1 - fp.ex0), (int)(fp.px_e - fp.ex0), (int)(fp.nx_s - fp.ex0),
-                          (int)fp.ex0, (int)fp.px_e, (int)fp.nx_s, (int)fp.ex1};
+                          (int)fp.ex0, (int)fp.px_e, (int)fp.nx_s, (int)fp.ex1,
+                          h->per_node ? h->h_wx.data() + (size_t)fp.fx * pl.nx : nullptr};
         const int64_t w = fp.ex1 - fp.ex0;
         for (int64_t r = 0; r < fp.ey1 - fp.ey0; ++r) {
             const float oy = omega_axis(ay, (int)r);
-            for (int64_t q = 0; q < w; ++q)
-                x[(fp.ey0 + r) * pl.nx + fp.ex0 + q] += oy * omega_axis(ax, (int)q) * xs[off[fp.id] + r * w + q];
+            for (int64_t q = 0; q < w; ++q) {
+                const float om = oy * omega_axis(ax, (int)q);
+                const int64_t o = (fp.ey0 + r) * pl.nx + fp.ex0 + q;
+                x[o] += om * xs[off[fp.id] + r * w + q];
+                if (h->per_node) wsum[o] += om;
+            }
         }
     }
+    if (h->per_node)
+        for (size_t i = 0; i < wsum.size(); ++i) x[i] /= wsum[i];
     return DEBLUR_OK;
 }
 
@@ -1146,6 +1232,13 @@ deblur_status deblur_kernel_work(deblur_t h, int32_t cls, double *flops, double 
         const FacetPlan &f = pl.facets[id];
         est_px += (double)(f.ey1 - f.ey0) * (f.ex1 - f.ex0);
         obs_px += (double)(f.oy1 - f.oy0) * (f.ox1 - f.ox0);
+        if (h->per_node) {     // one PSF per pixel: a = 1
+            if (cls == KC_H || cls == KC_H_OBJ || cls == KC_H_PLAIN)
+                *flops += 2.0 * P2 * (double)(f.oy1 - f.oy0) * (f.ox1 - f.ox0);
+            if (cls == KC_HT_UPDATE || cls == KC_HT_PLAIN)
+                *flops += 2.0 * P2 * (double)(f.ey1 - f.ey0) * (f.ex1 - f.ex0);
+            continue;
+        }
         if (cls == KC_H || cls == KC_H_OBJ || cls == KC_H_PLAIN)
             *flops += 2.0 * P2 * nz_sum(h->h_wy, h->prm.psf_gy, pl.ny, f.oy0 + c, f.oy1 + c) *
                       nz_sum(h->h_wx, h->prm.psf_gx, pl.nx, f.ox0 + c, f.ox1 + c);

@@ -17,9 +17,14 @@ struct AxisW {
     int b_next;          // local rows [b_next, n) are shared with the next facet (n = none)
     int s_prev, e_prev;  // global band with previous facet [s_prev, e_prev)
     int s_next, e_next;  // global band with next facet [s_next, e_next)
+    // per-node operator mode (alpha_i = gamma omega_i): omega along this
+    // axis is the facet's own interpolation weight row, indexed by the global
+    // coordinate (device pointer); NULL -> the A13 ramps above
+    const float *w;
 };
 
 __host__ __device__ inline float omega_axis(const AxisW &a, int t) {
+    if (a.w) return a.w[a.e0 + t];
     if (t < a.b_prev) return ((float)(a.e0 + t - a.s_prev) + 0.5f) / (float)(a.e_prev - a.s_prev);
     if (t >= a.b_next) return 1.0f - ((float)(a.e0 + t - a.s_next) + 0.5f) / (float)(a.e_next - a.s_next);
     return 1.0f;

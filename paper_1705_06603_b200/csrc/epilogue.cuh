@@ -116,7 +116,8 @@ __device__ __forceinline__ float update_value_t(const FacetDev &F, const float *
     }
     const float tdiv = dyu * sc_u - dyc * sc_c + dxl * sc_l - dxc * sc_c;
     shared = fy < F.ay.b_prev || fy >= F.ay.b_next || fx < F.ax.b_prev || fx >= F.ax.b_next;
-    const float om = shared ? omega_axis(F.ay, fy) * omega_axis(F.ax, fx) : 1.f;
+    // A13 ramps are 1 off the bands; per-node weights (F.ay.w) are not
+    const float om = (shared || F.ay.w) ? omega_axis(F.ay, fy) * omega_axis(F.ax, fx) : 1.f;
     const float gt = g + sc.lambda * tdiv + sc.gamma * om * (xc - uc);
     const float xn = fmaxf(0.f, xc - sc.tau * gt);
     u_new = uc + sc.rho * (xn - uc);

@@ -16,9 +16,11 @@ struct FftPlan;
 
 // Measured crossover: true when the FFT path beats the direct stencil for P.
 bool fft_prefer(int P);
+// d_wy/d_wx: the weights applied inside H_f (all ones in per-node mode, where every
+// tile of facet (a, b) uses PSF (a, b) only); h_wy/h_wx: the interpolation weights.
 FftPlan *fft_create(const Plan &pl, const std::vector<int> &local, const std::vector<FacetDev> &fh,
                     const float *d_psfs, const float *d_wy, const float *d_wx, int Gy, int Gx, const float *h_wy,
-                    const float *h_wx, cudaStream_t s, std::string &err);
+                    const float *h_wx, bool per_node, cudaStream_t s, std::string &err);
 void fft_destroy(FftPlan *f);
 // H on every local facet: mode RESIDUAL writes r = w (Hx - y) and data partials,
 // PLAIN writes r = Hx, OBJECTIVE only the partials.

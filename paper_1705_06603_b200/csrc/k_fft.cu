@@ -1319,7 +1319,7 @@ static cudaError_t do_attrs(int S, int T, int NP, int NQ) {
 
 FftPlan *fft_create(const Plan &pl, const std::vector<int> &local, const std::vector<FacetDev> &fh,
                     const float *d_psfs, const float *d_wy, const float *d_wx, int Gy, int Gx, const float *h_wy,
-                    const float *h_wx, cudaStream_t s, std::string &err) {
+                    const float *h_wx, bool per_node, cudaStream_t s, std::string &err) {
     FftPlan *f = new FftPlan();
     auto fail = [&](const std::string &m) { err = m; delete f; return (FftPlan *)nullptr; };
 #define FC(call)                                                                          \
@@ -1343,7 +1343,7 @@ FftPlan *fft_create(const Plan &pl, const std::vector<int> &local, const std::ve
     int LDF = 0, rows_nb = 0;
     if (do_geom(S, LDF, rows_nb) != cudaSuccess) return fail("bad FFT size");
     // active ranges
-    auto range = [](const float *w, int G, int64_t n, int64_t a, int64_t b, int &lo, int &hi) {
+    auto range_nz = [](const float *w, int G, int64_t n, int64_t a, int64_t b, int &lo, int &hi) {
         a = std::max<int64_t>(0, a); b = std::min<int64_t>(n, b);
         lo = G; hi = -1;
         for (int g = 0; g < G; ++g)
@@ -1353,6 +1353,14 @@ FftPlan *fft_create(const Plan &pl, const std::vector<int> &local, const std::ve
     std::vector<char> used(f->K, 0);
     for (size_t li = 0; li < fh.size(); ++li) {
         const FacetDev &F = fh[li];
+        // per-node operator mode: every tile of facet (a, b) uses PSF (a, b) alone
+        auto range = [&](const float *w, int G, int64_t n, int64_t a, int64_t b, int &lo, int &hi) {
+            if (per_node) {
+                lo = hi = (w == h_wy) ? pl.facets[F.id].fy : pl.facets[F.id].fx;
+                return;
+            }
+            range_nz(w, G, n, a, b, lo, hi);
+        };
         for (int y0 = 0; y0 < F.my; y0 += T)
             for (int x0 = 0; x0 < F.mx; x0 += T) {
                 TileDesc t{(int)li, y0, x0, 0, -1, 0, -1};

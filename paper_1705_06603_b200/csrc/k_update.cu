@@ -235,14 +235,21 @@ __global__ void k_x0_from_y(FacetDev F, const float *ydil, int64_t dpitch, int d
 }
 
 // image += omega^F_f . x_f over the facet's estimate block (A7); launched per facet in id order
-__global__ void k_blend(FacetDev F, int par, float *img, int64_t Nx) {
+// img += omega^F_f x_f (A7); wsum (per-node mode) += omega_f for the normalisation
+__global__ void k_blend(FacetDev F, int par, float *img, float *wsum, int64_t Nx) {
     const int64_t n = (int64_t)F.ny * F.nx;
     for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
         const int r = (int)(idx / F.nx), q = (int)(idx % F.nx);
         const float om = omega_axis(F.ay, r) * omega_axis(F.ax, q);
-        float *d = img + (int64_t)(F.ey0 + r) * Nx + F.ex0 + q;
-        *d += om * F.x[par][(int64_t)r * F.ep + q];
+        const int64_t o = (int64_t)(F.ey0 + r) * Nx + F.ex0 + q;
+        img[o] += om * F.x[par][(int64_t)r * F.ep + q];
+        if (wsum) wsum[o] += om;
     }
+}
+
+__global__ void k_normalize(float *img, const float *wsum, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        img[i] /= wsum[i];
 }
 
 }  // namespace
@@ -253,8 +260,13 @@ cudaError_t launch_x0_from_y(const FacetDev &F, const float *ydil, int64_t dpitc
     return cudaGetLastError();
 }
 
-cudaError_t launch_blend(const FacetDev &F, int par, float *img, int64_t Nx, cudaStream_t s) {
-    k_blend<<<1184, 256, 0, s>>>(F, par, img, Nx);
+cudaError_t launch_blend(const FacetDev &F, int par, float *img, float *wsum, int64_t Nx, cudaStream_t s) {
+    k_blend<<<1184, 256, 0, s>>>(F, par, img, wsum, Nx);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_normalize(float *img, const float *wsum, int64_t n, cudaStream_t s) {
+    k_normalize<<<1184, 256, 0, s>>>(img, wsum, n);
     return cudaGetLastError();
 }
 

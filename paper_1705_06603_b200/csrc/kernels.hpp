@@ -44,6 +44,7 @@ cudaError_t launch_maxdiff(const FacetDev *facets, const BandRect *rects, int nr
 
 cudaError_t launch_x0_from_y(const FacetDev &F, const float *ydil, int64_t dpitch, int dy0, int dx0, int My, int Mx,
                              int c, cudaStream_t s);
-cudaError_t launch_blend(const FacetDev &F, int par, float *img, int64_t Nx, cudaStream_t s);
+cudaError_t launch_blend(const FacetDev &F, int par, float *img, float *wsum, int64_t Nx, cudaStream_t s);
+cudaError_t launch_normalize(float *img, const float *wsum, int64_t n, cudaStream_t s);
 
 }  // namespace deblur

@@ -15,7 +15,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "libdeblur.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
+OP_INTERP, OP_PER_NODE = 0, 1
 CONV_AUTO, CONV_DIRECT, CONV_FFT = 0, 1, 2
 STATUS = {0: "DEBLUR_OK", -1: "DEBLUR_EINVAL", -2: "DEBLUR_ESHAPE", -3: "DEBLUR_ENOMEM", -4: "DEBLUR_ECUDA",
           -5: "DEBLUR_ENCCL", -6: "DEBLUR_ENUMERIC", -7: "DEBLUR_ESTATE"}
@@ -42,6 +43,7 @@ class Params(ctypes.Structure):
         ("conv_path", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
         ("device", ctypes.c_int32),
         ("nccl_id", ctypes.c_void_p),
+        ("operator_mode", ctypes.c_int32),
     ]
 
 
@@ -133,7 +135,7 @@ def make_params(psfs, wy, wx, y, noise_w=None, noise_w_scalar: float = 1.0, lam:
                 eps: float = 1e-3, reg_kind: int = 0, tv_boundary: int = 0, gamma: float = 0.0, rho: float = 1.0,
                 tau: float = 0.0, inner_steps: int = 1, facet_gy: int = 1, facet_gx: int = 1, overlap: int = 0,
                 x0=None, conv_path: int = CONV_AUTO, rank: int = 0, world: int = 1, device: int = 0,
-                nccl_id_bytes: Optional[bytes] = None):
+                nccl_id_bytes: Optional[bytes] = None, operator_mode: int = 0):
     """Returns (Params, keepalive) -- keepalive holds the arrays the pointers refer to."""
     psfs = _f32(psfs)
     wy, wx, y = _f32(wy), _f32(wx), _f32(y)
@@ -158,7 +160,8 @@ def make_params(psfs, wy, wx, y, noise_w=None, noise_w_scalar: float = 1.0, lam:
                noise_w_scalar=noise_w_scalar, lam=lam, eps=eps, reg_kind=reg_kind, tv_boundary=tv_boundary,
                gamma=gamma, rho=rho, tau=tau, inner_steps=inner_steps, facet_gy=facet_gy, facet_gx=facet_gx,
                overlap=overlap, x0=_ptr(x0a), conv_path=conv_path, rank=rank, world=world, device=device,
-               nccl_id=ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None)
+               nccl_id=ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None,
+               operator_mode=operator_mode)
     return p, keep
 
 
@@ -166,7 +169,8 @@ def problem_params(pb, **over):
     """make_params for a synth.Problem (same field names)."""
     kw = dict(noise_w=pb.noise_w, noise_w_scalar=pb.noise_w_scalar, lam=pb.lam, eps=pb.eps,
               reg_kind=pb.reg_kind, tv_boundary=pb.tv_boundary, gamma=pb.gamma, rho=pb.rho,
-              inner_steps=pb.inner_steps, facet_gy=pb.fy, facet_gx=pb.fx, overlap=pb.overlap, x0=pb.x0)
+              inner_steps=pb.inner_steps, facet_gy=pb.fy, facet_gx=pb.fx, overlap=pb.overlap, x0=pb.x0,
+              operator_mode=getattr(pb, "operator_mode", 0))
     kw.update(over)
     return make_params(pb.psfs, pb.wy, pb.wx, pb.y, **kw)
 

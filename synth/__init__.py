@@ -32,7 +32,7 @@ from typing import Optional
 
 import numpy as np
 
-__all__ = ["Problem", "CONFIGS", "make_config", "make_problem", "hat_weights",
+__all__ = ["Problem", "CONFIGS", "make_config", "make_problem", "per_node", "hat_weights",
            "psf_grid", "render_observed", "render_scene"]
 
 
@@ -62,6 +62,7 @@ class Problem:
     overlap: int = 0
     iters: int = 20
     x0: Optional[np.ndarray] = None
+    operator_mode: int = 0    # 0: interpolated H restricted to facets; 1: per-node PSFs
 
     @property
     def my(self) -> int:
@@ -358,3 +359,18 @@ def make_config(k: int, n: Optional[int] = None, **over) -> Problem:
         cfg["n"] = n
     cfg.update(over)
     return make_problem(name=f"c{k}" + ("" if n in (None, full_n) else f"@{n}"), seed=1000 * k, **cfg)
+
+
+def per_node(pb: Problem, overlap: Optional[int] = None) -> Problem:
+    """The paper's node geometry for a problem: one facet per
+    PSF grid point (F = G), each facet deblurred with its own PSF only and
+    consensus weights = its interpolation weights (operator_mode 1).  The default
+    overlap is the largest the facet planner admits (every estimate pixel in at
+    most two facets per axis: O <= floor(M/F) - (P - 1), even), so each block
+    spans about three grid points as in PAPER.md:255."""
+    if overlap is None:
+        core = min(pb.my // pb.gy, pb.mx // pb.gx)
+        overlap = max(0, core - (pb.P - 1))
+        overlap -= overlap % 2
+    return dataclasses.replace(pb, fy=pb.gy, fx=pb.gx, overlap=int(overlap), operator_mode=1,
+                               name=pb.name + "-node")

@@ -286,3 +286,22 @@ def test_iterate_traced(path):
             assert abs(tr[k, i] - ref[k][i]) <= OBJ_TOL * abs(ref[k][i]) + 1e-12, (k, i, tr[k, i], ref[k][i])
         assert abs(tr[k, 3] - ref[k][3]) <= IT_TOL * max(1.0, np.abs(xr).max())
     assert tr[3, 0] < tr[0, 0]              # the objective decreases from the A6 start
+
+
+# ------------------------------------------------------------------ per-node operator mode (NEXT-2)
+@pytest.mark.parametrize("path", PATHS, ids=["direct", "fft"])
+@pytest.mark.parametrize("k,n", [(2, 300), (1, 256), (3, 700)])
+def test_iterate_per_node(k, n, path):
+    """operator_mode 1: facet (a, b) deblurs with PSF
+    (a, b) alone, alpha_f = gamma omega_f with the interpolation weights, the
+    image is the normalised omega-blend -- iterate, objective and image vs the
+    oracle's per-node mode."""
+    pb = synth.per_node(synth.make_config(k, n=n))
+    check_pair(run_pair(pb, 5, path))
+
+
+def test_per_node_rejects_mismatched_grid():
+    pb = synth.make_config(2, n=300)
+    with pytest.raises(D.DeblurError) as e:
+        D.Deblur.from_problem(pb, operator_mode=D.OP_PER_NODE)      # 2x2 facets, 4x4 PSFs
+    assert "facet grid" in str(e.value)
