@@ -110,6 +110,8 @@ def run_ours(args, rank, world, local):
         import torch.distributed as dist
         dist.init_process_group("gloo")
     pb = synth.make_config(args.config)
+    if args.operator_mode == 1:
+        pb = synth.per_node(pb)
     nid = None
     if world > 1:
         import torch.distributed as dist
@@ -242,6 +244,8 @@ def run_ours(args, rank, world, local):
                        "psf_grid": f"{pb.gy}x{pb.gx}", "facets": f"{pb.fy}x{pb.fx}", "overlap": pb.overlap,
                        "lambda": pb.lam, "eps": pb.eps, "iterations_per_step": 1, "inner_steps": pb.inner_steps,
                        "conv_path": {1: "direct", 2: "fft"}[dev.conv_path],
+                       "operator_mode": {0: "interpolated H per facet", 1: "per-node PSFs (paper node model)"}[
+                           args.operator_mode],
                        "l2": "no flush: resident state >> 126 MB L2", "parallelism": f"facets over {world} GPU(s)"},
             "gpu_launches": int(launches),
             "roofline": roofline,
@@ -325,6 +329,8 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--path", choices=["auto", "direct", "fft"], default="auto")
+    ap.add_argument("--operator-mode", type=int, choices=[0, 1], default=0,
+                    help="0: interpolated H restricted to facets (north star); 1: per-node PSFs, facets = PSF grid")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-crop", type=int, default=1024)

@@ -150,7 +150,9 @@ DEBLUR_API deblur_status deblur_create(const deblur_params *p, deblur_t *out);
 DEBLUR_API deblur_status deblur_destroy(deblur_t h);
 
 /* hx = H x on the whole image.  x: host [N_y][N_x]; hx: host
- * [M_y][M_x], written on rank 0.  Facet-wise, owner computes (§8b).  COLLECTIVE. */
+ * [M_y][M_x], written on rank 0.  Facet-wise, owner computes (§8b).  In the
+ * per-node operator mode each observed pixel takes the local operator H_f of the
+ * facet owning it (the piecewise shift-invariant model of P:109).  COLLECTIVE. */
 DEBLUR_API deblur_status deblur_apply_H(deblur_t h, const float *x, float *hx);
 /* g = H^T r (adjoint).  r: host [M_y][M_x]; g: host [N_y][N_x] on rank 0.
  * Requires overlap >= P-1 when there is more than one facet (else EINVAL).  COLLECTIVE. */

@@ -71,6 +71,8 @@ struct deblur_ctx {
     TileDesc *d_tilesH = nullptr, *d_tilesHT = nullptr;
     std::vector<BandRect> rects;
     BandRect *d_rects = nullptr;
+    std::vector<RectTile> rect_tiles;
+    RectTile *d_rect_tiles = nullptr;
     double *d_partials = nullptr;
     std::vector<double> h_partials;
     SolverConst sc{};
@@ -672,15 +674,21 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
                         }
                 }
             }
-        // band rectangles (facet-local): pixels in >= 2 facets
-        const int by0 = F.ay.b_prev, by1 = F.ay.b_next, bx0 = F.ax.b_prev, bx1 = F.ax.b_next;
-        auto add = [&](int y0, int y1, int x0, int x1) {
-            if (y1 > y0 && x1 > x0) h->rects.push_back({(int)li, y0, y1, x0, x1});
-        };
-        add(0, by0, 0, F.nx);
-        add(by1, F.ny, 0, F.nx);
-        add(by0, by1, 0, bx0);
-        add(by0, by1, bx1, F.nx);
+        // band rectangles (facet-local): pixels in >= 2 facets, split into the 8 pieces
+        // of the 3 x 3 (previous band | core | next band) grid around the core, so the
+        // set of contributing neighbours is constant on each piece
+        const int rb[4] = {0, F.ay.b_prev, F.ay.b_next, F.ny}, cb[4] = {0, F.ax.b_prev, F.ax.b_next, F.nx};
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) {
+                if (a == 1 && b == 1) continue;                    // single-owner core
+                if (rb[a + 1] <= rb[a] || cb[b + 1] <= cb[b]) continue;
+                const BandRect R{(int)li, rb[a], rb[a + 1], cb[b], cb[b + 1],
+                                 a == 0 ? -1 : 0, a == 2 ? 1 : 0, b == 0 ? -1 : 0, b == 2 ? 1 : 0};
+                const int ri = (int)h->rects.size();
+                h->rects.push_back(R);
+                for (int y = R.y0; y < R.y1; y += 8)
+                    for (int x = R.x0; x < R.x1; x += 256) h->rect_tiles.push_back({ri, y, x});
+            }
     }
 
     // tiles with active PSF ranges
@@ -717,6 +725,10 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
     CUC(cudaMemcpy(h->d_tilesH, h->tilesH.data(), sizeof(TileDesc) * h->tilesH.size(), cudaMemcpyHostToDevice));
     CUC(cudaMemcpy(h->d_tilesHT, h->tilesHT.data(), sizeof(TileDesc) * h->tilesHT.size(), cudaMemcpyHostToDevice));
     CUC(cudaMemcpy(h->d_rects, h->rects.data(), sizeof(BandRect) * h->rects.size(), cudaMemcpyHostToDevice));
+    CUC(h->dalloc(&h->d_rect_tiles, std::max<size_t>(1, h->rect_tiles.size())));
+    if (!h->rect_tiles.empty())
+        CUC(cudaMemcpy(h->d_rect_tiles, h->rect_tiles.data(), sizeof(RectTile) * h->rect_tiles.size(),
+                       cudaMemcpyHostToDevice));
     const size_t npart = std::max({h->tilesH.size(), h->tilesHT.size(), h->rects.size(), (size_t)1});
     CUC(h->dalloc(&h->d_partials, npart));
     h->h_partials.resize(npart);
@@ -771,7 +783,8 @@ static deblur_status one_iteration(deblur_t h) {
     if ((s = exchange(h, 0)) != DEBLUR_OK) return s;
     cudaEvent_t ev = nullptr;
     h->prof_begin(KC_CONSENSUS, &ev);
-    CU(launch_consensus(h->d_facets, h->d_rects, (int)h->rects.size(), h->par, h->sc.rho, h->stream));
+    CU(launch_consensus(h->d_facets, h->d_rects, h->d_rect_tiles, (int)h->rect_tiles.size(), h->par, h->sc.rho,
+                        h->stream));
     h->prof_end(KC_CONSENSUS, ev);
     return DEBLUR_OK;
 }

@@ -75,6 +75,11 @@ struct TileDesc {         // one CTA's tile
 struct BandRect {         // consensus work item: facet-local rectangle of band pixels
     int f;
     int y0, y1, x0, x1;
+    int dy0, dy1, dx0, dx1;   // the neighbour offsets contributing on the whole rectangle
+};
+
+struct RectTile {         // consensus launch unit: 8 rows x 256 columns of one BandRect
+    int rect, y0, x0;
 };
 
 struct SolverConst {

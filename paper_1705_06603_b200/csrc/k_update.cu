@@ -113,6 +113,8 @@ __global__ void __launch_bounds__(EPI_NT, K4_MINB) k_update_from_g(const FacetDe
         if (last) {
             if (full && !sh[0] && !sh[1] && !sh[2] && !sh[3]) {
                 *reinterpret_cast<float4 *>(up + o) = make_float4(nu[0], nu[1], nu[2], nu[3]);
+            } else if (full && sh[0] && sh[1] && sh[2] && sh[3]) {
+                *reinterpret_cast<float4 *>(vp + o) = make_float4(nv[0], nv[1], nv[2], nv[3]);
             } else {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
@@ -163,29 +165,71 @@ __device__ __forceinline__ float view_at(const View &v, int par, int gy, int gx)
     return v.base[par][(int64_t)(gy - v.y0) * v.pitch + (gx - v.x0)];
 }
 
-// grid: x = chunks of 256 pixels, y = rect index
-__global__ void __launch_bounds__(256) k_consensus(const FacetDev *facets, const BandRect *rects, int par, float rho) {
-    const BandRect R = rects[blockIdx.y];
+// one CTA per RectTile (8 rows x 256 columns of a band piece).  The contributing
+// neighbour offsets are constant on the piece: their descriptors (v pointer at this
+// column, pitch, omega along x) and the 8 rows' omega along y are resolved once per
+// thread, so the row loop is loads + arithmetic only.
+__global__ void __launch_bounds__(256) k_consensus(const FacetDev *facets, const BandRect *rects,
+                                                   const RectTile *tiles, int par, float rho) {
+    const RectTile T = tiles[blockIdx.x];
+    const BandRect R = rects[T.rect];
     const FacetDev &F = facets[R.f];
-    const int w = R.x1 - R.x0;
-    const int64_t n = (int64_t)(R.y1 - R.y0) * w;
-    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
-        const int ly = R.y0 + (int)(idx / w), lx = R.x0 + (int)(idx % w);
-        const int gy = F.ey0 + ly, gx = F.ex0 + lx;
-        const int dy0 = (ly < F.ay.b_prev) ? -1 : 0, dy1 = (ly >= F.ay.b_next) ? 1 : 0;
-        const int dx0 = (lx < F.ax.b_prev) ? -1 : 0, dx1 = (lx >= F.ax.b_next) ? 1 : 0;
+    const int lx = T.x0 + (int)threadIdx.x;
+    if (lx >= R.x1) return;
+    const int gx = F.ex0 + lx;
+    const int gy0 = F.ey0 + T.y0;
+    const int nr = min(8, R.y1 - T.y0);
+    const int ndx = R.dx1 - R.dx0 + 1, nc = (R.dy1 - R.dy0 + 1) * ndx;
+    const float *vp[4];
+    int64_t vpitch[4];
+    float omx[4];
+    float omy[2][8];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        vp[c] = nullptr; vpitch[c] = 0; omx[c] = 0.f;
+        if (c < nc) {
+            const int dy = R.dy0 + c / ndx, dx = R.dx0 + c % ndx;     // ascending facet id (A9)
+            const Neighbour &nb = F.nb[dy + 1][dx + 1];
+            vpitch[c] = nb.v.pitch;
+            vp[c] = nb.v.base[par] + (int64_t)(gy0 - nb.v.y0) * nb.v.pitch + (gx - nb.v.x0);
+            omx[c] = omega_axis(nb.ax, gx - nb.ax.e0);
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+        const int dy = R.dy0 + a;
+        const Neighbour &nb = F.nb[min(dy, 1) + 1][R.dx0 + 1];
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+            omy[a][r] = (dy <= R.dy1 && r < nr) ? omega_axis(nb.ay, gy0 + r - nb.ay.e0) : 0.f;
+    }
+    float *__restrict__ up = F.u + (int64_t)T.y0 * F.ep + lx;
+    const float *__restrict__ xp = F.x[par] + (int64_t)T.y0 * F.ep + lx;
+    // every load of the 8 rows in flight before the first use (v / x through the
+    // read-only path: the u stores cannot alias them)
+    float vv[8][4], xv[8], uv[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        const bool ok = r < nr;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) vv[r][c] = (ok && c < nc) ? __ldg(vp[c] + (int64_t)r * vpitch[c]) : 0.f;
+        xv[r] = ok ? __ldg(xp + (int64_t)r * F.ep) : 0.f;
+        uv[r] = ok ? up[(int64_t)r * F.ep] : 0.f;
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        if (r >= nr) break;
         float num = 0.f, den = 0.f;
-        // ascending facet id = lexicographic (dy, dx) (A9)
-        for (int dy = dy0; dy <= dy1; ++dy)
-            for (int dx = dx0; dx <= dx1; ++dx) {
-                const Neighbour &nb = F.nb[dy + 1][dx + 1];
-                const float om = omega_axis(nb.ay, gy - nb.ay.e0) * omega_axis(nb.ax, gx - nb.ax.e0);
-                num += om * view_at(nb.v, par, gy, gx);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            if (c < nc) {
+                const float om = omy[c / ndx][r] * omx[c];
+                num += om * vv[r][c];
                 den += om;
             }
+        }
         const float zbar = num / den;
-        const int64_t o = (int64_t)ly * F.ep + lx;
-        F.u[o] += rho * (zbar - F.x[par][o]);
+        up[(int64_t)r * F.ep] = uv[r] + rho * (zbar - xv[r]);
     }
 }
 
@@ -291,11 +335,10 @@ cudaError_t launch_tv_value(const FacetDev *facets, const TileDesc *tiles, int n
     return cudaGetLastError();
 }
 
-cudaError_t launch_consensus(const FacetDev *facets, const BandRect *rects, int nrect, int par, float rho,
-                             cudaStream_t s) {
-    if (!nrect) return cudaSuccess;
-    dim3 grid(64, nrect);
-    k_consensus<<<grid, 256, 0, s>>>(facets, rects, par, rho);
+cudaError_t launch_consensus(const FacetDev *facets, const BandRect *rects, const RectTile *tiles, int ntiles,
+                             int par, float rho, cudaStream_t s) {
+    if (!ntiles) return cudaSuccess;
+    k_consensus<<<ntiles, 256, 0, s>>>(facets, rects, tiles, par, rho);
     return cudaGetLastError();
 }
 

@@ -35,8 +35,8 @@ cudaError_t launch_HT_direct(const ConvArgs &a, int mode, int par, int last_step
 // k_update.cu: elementwise / band kernels
 cudaError_t launch_update_from_g(const FacetDev *facets, const TileDesc *tiles, int ntiles, int P, int par,
                                  int last_step, const SolverConst &sc, double *partials, cudaStream_t s);
-cudaError_t launch_consensus(const FacetDev *facets, const BandRect *rects, int nrect, int par, float rho,
-                             cudaStream_t s);
+cudaError_t launch_consensus(const FacetDev *facets, const BandRect *rects, const RectTile *tiles, int ntiles,
+                             int par, float rho, cudaStream_t s);
 cudaError_t launch_tv_value(const FacetDev *facets, const TileDesc *tiles, int ntiles, int P, int par,
                             const SolverConst &sc, double *partials, cudaStream_t s);
 cudaError_t launch_maxdiff(const FacetDev *facets, const BandRect *rects, int nrect, int par, double *partials,
