@@ -138,6 +138,10 @@ typedef struct {
     int32_t rank, world, device;  /* SPMD rank / world size; CUDA device ordinal */
     const void *nccl_id;          /* 128-byte ncclUniqueId identical on all ranks; NULL if world == 1 */
     int32_t operator_mode;        /* deblur_operator_mode (default DEBLUR_OP_INTERP) */
+    int32_t independent;          /* 1: the paper's "independent" baseline (NEXT-3): every
+                                     facet solves its own problem, no consensus, no halo exchange,
+                                     alpha = 0 (gamma is ignored, also in the default tau);
+                                     get_image blends with omega^F.  0: Algorithm 1 (default) */
 } deblur_params;
 
 /* 128-byte NCCL unique id for a world > 1 run: call on rank 0, broadcast

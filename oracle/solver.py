@@ -15,6 +15,8 @@ with the readings of SURVEY §8c:
   A8/A9  consensus divides by the computed sum of weights, facets in ascending id
   A20    every facet uses its full W_i (no multiplicity division)
   A22    objective = sum_f [data_f + lambda reg_f] at the current x (+ max |x_i - x_j|)
+Independent baseline (NEXT-3): every facet runs the Local-Solver on
+  its own f_i with alpha = 0 (gamma := 0, also in tau) and no consensus; image as A7.
 Operator modes (NEXT-2):
   0  H_i = the global PSF-interpolation H (PAPER.md:107) restricted to facet i (R1);
      omega_i = the A13 ramps (partition of unity on every band)
@@ -96,8 +98,12 @@ class Deblur:
     """Oracle state for one problem: per-facet x_f, u_f (fp64)."""
 
     def __init__(self, psfs, wy, wx, y, w, Fy: int, Fx: int, overlap: int, params: Params,
-                 tau: Optional[float] = None, x0: Optional[np.ndarray] = None, operator_mode: int = 0):
+                 tau: Optional[float] = None, x0: Optional[np.ndarray] = None, operator_mode: int = 0,
+                 independent: bool = False):
         self.op = Operator(psfs, wy, wx)
+        self.independent = bool(independent)
+        if self.independent:      # the paper's independent baseline (P:266, P:296): alpha = 0, no consensus
+            params = dataclasses.replace(params, gamma=0.0)
         self.prm = params
         self.operator_mode = int(operator_mode)
         self.y = np.asarray(y, np.float64)
@@ -158,8 +164,11 @@ class Deblur:
     # ---- Algorithm 1 ------------------------------------------------------
     def iterate(self, n: int = 1):
         for _ in range(n):
-            self.x, self.u = dr_iteration(self.shape, self.windows, self.omegas, self.x, self.u,
-                                          self.local_prox, self.prm.rho)
+            if self.independent:
+                self.x = [self.local_prox(i, self.x[i], self.u[i]) for i in range(len(self.windows))]
+            else:
+                self.x, self.u = dr_iteration(self.shape, self.windows, self.omegas, self.x, self.u,
+                                              self.local_prox, self.prm.rho)
         return self
 
     # ---- diagnostics ------------------------------------------------------
@@ -206,4 +215,4 @@ def from_problem(pb, tau: Optional[float] = None, **over) -> Deblur:
         setattr(prm, k, v)
     w = pb.noise_w if pb.noise_w is not None else np.float64(np.float32(pb.noise_w_scalar))
     return Deblur(pb.psfs, pb.wy, pb.wx, pb.y, w, pb.fy, pb.fx, pb.overlap, prm, tau=tau, x0=pb.x0,
-                  operator_mode=getattr(pb, "operator_mode", 0))
+                  operator_mode=getattr(pb, "operator_mode", 0), independent=bool(getattr(pb, "independent", 0)))

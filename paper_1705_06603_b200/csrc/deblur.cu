@@ -202,6 +202,7 @@ deblur_status validate(const deblur_params *p, std::string &err) {
     if (p->world < 1 || p->rank < 0 || p->rank >= p->world) { err = "rank/world out of range"; return DEBLUR_EINVAL; }
     if (p->world > 1 && !p->nccl_id) { err = "nccl_id is NULL with world > 1"; return DEBLUR_EINVAL; }
     if (!(std::isfinite(p->tau))) { err = "tau must be finite"; return DEBLUR_EINVAL; }
+    if (p->independent != 0 && p->independent != 1) { err = "independent must be 0 or 1"; return DEBLUR_EINVAL; }
     if (p->operator_mode != DEBLUR_OP_INTERP && p->operator_mode != DEBLUR_OP_PER_NODE) {
         err = "operator_mode must be 0 (interpolated H) or 1 (per-node PSFs)";
         return DEBLUR_EINVAL;
@@ -279,7 +280,8 @@ double default_tau(const deblur_params *p) {
         wmax = (double)p->noise_w_scalar;
     }
     const double lip = (p->reg_kind == 0) ? 1.0 / (double)p->eps : 1.0;
-    const double L = wmax * S * S * a_row * a_col + (double)p->lambda * 8.0 * lip + (double)p->gamma;
+    const double gamma = p->independent ? 0.0 : (double)p->gamma;     // independent: alpha = 0
+    const double L = wmax * S * S * a_row * a_col + (double)p->lambda * 8.0 * lip + gamma;
     return L > 0 ? 1.0 / L : 1.0;
 }
 
@@ -744,7 +746,7 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
 
     // solver constants
     h->tau = (p->tau > 0) ? p->tau : default_tau(p);
-    h->sc.lambda = p->lambda; h->sc.eps = p->eps; h->sc.gamma = p->gamma; h->sc.rho = p->rho;
+    h->sc.lambda = p->lambda; h->sc.eps = p->eps; h->sc.gamma = p->independent ? 0.f : p->gamma; h->sc.rho = p->rho;
     h->sc.tau = (float)h->tau; h->sc.reg_kind = p->reg_kind; h->sc.tv_boundary = p->tv_boundary;
 
     // data + initial state
@@ -779,7 +781,9 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
 static deblur_status one_iteration(deblur_t h) {
     deblur_status s;
     for (int k = 0; k < h->prm.inner_steps; ++k)
-        if ((s = local_step(h, k == h->prm.inner_steps - 1)) != DEBLUR_OK) return s;
+        // independent baseline: no dual / band values either (u stays u0, v unused)
+        if ((s = local_step(h, k == h->prm.inner_steps - 1 && !h->prm.independent)) != DEBLUR_OK) return s;
+    if (h->prm.independent) return DEBLUR_OK;        // baseline: no exchange, no consensus
     if ((s = exchange(h, 0)) != DEBLUR_OK) return s;
     cudaEvent_t ev = nullptr;
     h->prof_begin(KC_CONSENSUS, &ev);

@@ -24,6 +24,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include <cuda_pipeline.h>
@@ -1231,17 +1232,32 @@ static size_t smem_rows_inv(int NQ, bool ht = true) {
     return (size_t)S * 8 + (size_t)G::NB * G::RS * 8 + (size_t)G::NB * C2R<S>::SS * 8 + (ht ? (size_t)NQ * S * 4 : 0);
 }
 
+// The dynamic-shared-memory limit is a property of the kernel function, shared by
+// every handle in the process: only ever raise it (handles of different geometry
+// need different sizes; lowering it would break a live handle's launches).
+static std::mutex g_attr_mu;
+template <typename K>
+static cudaError_t raise_smem(K kern, size_t bytes) {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return e;
+    if ((size_t)fa.maxDynamicSharedSizeBytes >= bytes) return cudaSuccess;
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
 template <int S>
 static cudaError_t setup_attrs(int T, int NP, int NQ) {
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(k_rows_fwd<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rows_fwd<S>())) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(k_cols<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cols<S>(NP, NQ))) != cudaSuccess) return e;
+    (void)T;
+    if ((e = raise_smem(k_rows_fwd<S>, smem_rows_fwd<S>())) != cudaSuccess) return e;
+    if ((e = raise_smem(k_cols<S>, smem_cols<S>(NP, NQ))) != cudaSuccess) return e;
 #if COLS_TMEM
     if constexpr (S == 512)
-        if ((e = cudaFuncSetAttribute(k_cols_tm<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cols_tm<S>(NP, NQ))) != cudaSuccess) return e;
+        if ((e = raise_smem(k_cols_tm<S>, smem_cols_tm<S>(NP, NQ))) != cudaSuccess) return e;
 #endif
-    if ((e = cudaFuncSetAttribute(k_rows_inv<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rows_inv<S>(NQ, false))) != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_rows_inv<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_rows_inv<S>(NQ));
+    if ((e = raise_smem(k_rows_inv<S, false>, smem_rows_inv<S>(NQ, false))) != cudaSuccess) return e;
+    return raise_smem(k_rows_inv<S, true>, smem_rows_inv<S>(NQ));
 }
 
 template <int S>

@@ -63,6 +63,7 @@ class Problem:
     iters: int = 20
     x0: Optional[np.ndarray] = None
     operator_mode: int = 0    # 0: interpolated H restricted to facets; 1: per-node PSFs
+    independent: int = 0      # 1: the paper's independent baseline (no consensus, alpha = 0)
 
     @property
     def my(self) -> int:

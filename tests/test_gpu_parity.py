@@ -305,3 +305,31 @@ def test_per_node_rejects_mismatched_grid():
     with pytest.raises(D.DeblurError) as e:
         D.Deblur.from_problem(pb, operator_mode=D.OP_PER_NODE)      # 2x2 facets, 4x4 PSFs
     assert "facet grid" in str(e.value)
+
+
+@pytest.mark.parametrize("path", PATHS, ids=["direct", "fft"])
+@pytest.mark.parametrize("node", [0, 1], ids=["interp", "per_node"])
+def test_iterate_independent(node, path):
+    """The independent baseline (no consensus, alpha = 0) vs the oracle."""
+    pb = synth.make_config(2, n=300, facets=(2, 2), overlap=40)
+    if node:
+        pb = synth.per_node(pb)
+    pb.independent = 1
+    check_pair(run_pair(pb, 5, path))
+
+
+def test_two_live_handles_of_different_geometry():
+    """Kernel attributes (dynamic shared-memory limits) are process-wide: a second
+    handle with smaller tiles must not break a live one (regression)."""
+    pa = synth.make_config(2, n=300, facets=(1, 1), overlap=0)
+    pb = synth.per_node(synth.make_config(2, n=300))
+    with D.Deblur.from_problem(pa, conv_path=D.CONV_FFT) as ref:
+        ref.iterate(3)
+        xr, _ = ref.get_state()
+    with D.Deblur.from_problem(pa, conv_path=D.CONV_FFT) as a:
+        with D.Deblur.from_problem(pb, conv_path=D.CONV_FFT) as b:
+            b.iterate(2)
+        a.iterate(3)
+        xa, _ = a.get_state()
+        a.objective()
+    np.testing.assert_array_equal(xa, xr)

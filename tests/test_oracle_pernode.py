@@ -12,6 +12,8 @@ node), :206 (alpha_i = gamma omega_i with omega_i the interpolation weights).
               weights) step by step
   fixed pt.   the D-R fixed point equals argmin_{x >= 0} sum_i f_i(R_i x) with the
               per-node dense operators (scipy L-BFGS-B)
+and of the independent baseline (NEXT-3): one facet = Algorithm 1
+with gamma = 0; on several facets every facet equals its own one-facet problem.
 """
 import numpy as np
 import scipy.optimize
@@ -122,3 +124,33 @@ def test_per_node_synth_geometry():
         assert pl[k - 1].e_hi <= pl[k + 1].e_lo
     cell = pb.ny / pb.gy
     assert all((f.e_hi - f.e_lo) > 1.5 * cell for f in pl[1:-1])
+
+
+# --------------------------------------------------------- independent baseline (NEXT-3)
+def test_independent_single_facet_equals_dr_with_gamma0():
+    """One facet: the independent baseline (alpha = 0, no consensus) is Algorithm 1
+    with gamma = 0 step by step (the prox term vanishes, u never enters)."""
+    psfs, wy, wx, y, w, prm, _ = tiny_nodes(n=24, P=5, G=2, lam=0.05, eps=0.2, seed=11)
+    import dataclasses
+    a = Deblur(psfs, wy, wx, y, w, 1, 1, 0, dataclasses.replace(prm, gamma=0.0))
+    b = Deblur(psfs, wy, wx, y, w, 1, 1, 0, prm, independent=True)
+    assert a.tau == b.tau
+    a.iterate(6)
+    b.iterate(6)
+    np.testing.assert_array_equal(a.x[0], b.x[0])
+
+
+def test_independent_facets_are_separate_problems():
+    """Independent baseline on 2x2 facets: facet i's iterates equal a one-facet
+    problem on facet i's own data (its observed block, the weights restricted
+    to its estimate block) -- the blocks never talk."""
+    psfs, wy, wx, y, w, prm, _ = tiny_nodes(n=40, P=5, G=2, lam=0.05, eps=0.2, seed=12)
+    d = Deblur(psfs, wy, wx, y, w, 2, 2, 6, prm, independent=True)
+    d.iterate(5)
+    for i, f in enumerate(d.facets):
+        s = Deblur(psfs, wy[:, f.ey[0]:f.ey[1]], wx[:, f.ex[0]:f.ex[1]], y[f.oy[0]:f.oy[1], f.ox[0]:f.ox[1]],
+                   w[f.oy[0]:f.oy[1], f.ox[0]:f.ox[1]], 1, 1, 0, prm, tau=d.tau,
+                   x0=np.maximum(0.0, np.pad(y, 2, mode="edge"))[f.ey[0]:f.ey[1], f.ex[0]:f.ex[1]],   # A6
+                   independent=True)
+        s.iterate(5)
+        np.testing.assert_allclose(d.x[i], s.x[0], rtol=0, atol=1e-13)
