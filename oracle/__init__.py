@@ -10,6 +10,7 @@ Contents (each function cites the PAPER.md passage it follows):
   geometry.py              facet index sets and omega^F
   tv.py                    D, phi, psi (smoothed TV / Huber)
   solver.py                Algorithm 1 with Lemma 1
+  vmlmb.py                 VMLM-B Local-Solver (reading V1-V6) PAPER.md:287, :290
 
 Pins (tests/test_oracle_*.py, -m "not gpu") tie every function to something
 other than itself; see DESIGN.md §4 for the table.  "parity unpinned": the

@@ -33,7 +33,7 @@ from typing import Callable, List, Optional, Sequence, Tuple
 
 import numpy as np
 
-from . import geometry, tv
+from . import geometry, tv, vmlmb
 from .operators import Operator
 
 
@@ -92,6 +92,8 @@ class Params:
     reg_kind: int = 0
     tv_boundary: int = 0
     inner_steps: int = 1
+    local_solver: int = 0        # 0: K_in projected-gradient steps (R2); 1: VMLM-B (V1-V6, vmlmb.py)
+    inner_increment: int = 0     # VMLM-B budget at outer iteration k: inner_steps + k * inner_increment
 
 
 class Deblur:
@@ -133,6 +135,7 @@ class Deblur:
         x0 = np.asarray(x0, np.float64)
         self.x = [x0[win].copy() for win in self.windows]
         self.u = [x0[win].copy() for win in self.windows]
+        self.k = 0                                        # outer iteration counter (VMLM-B budget)
 
     @property
     def shape(self):
@@ -155,8 +158,27 @@ class Deblur:
         g = g + p.gamma * self.omegas[i] * (xi - ui)
         return g
 
+    def local_value_grad(self, i: int, w: np.ndarray, ui: np.ndarray):
+        """f_i(w) + 1/2 |w - u_i|^2_{alpha_i} (without the indicator) and its gradient."""
+        f = self.facets[i]
+        p = self.prm
+        d = self.ops[i].H_window(w, f.ey[0], f.ex[0]) - self.y[self.owin[i]]
+        wd = self.w[self.owin[i]] * d
+        al = p.gamma * self.omegas[i]
+        val = 0.5 * float((wd * d).sum()) + p.lam * tv.value(w, p.eps, p.reg_kind, p.tv_boundary) \
+            + 0.5 * float((al * (w - ui) ** 2).sum())
+        g = self.ops[i].HT_window(wd, f.ey[0], f.ex[0]) + p.lam * tv.grad(w, p.eps, p.reg_kind, p.tv_boundary) \
+            + al * (w - ui)
+        return val, g
+
     def local_prox(self, i: int, xi: np.ndarray, ui: np.ndarray) -> np.ndarray:
-        """Local-Solver (R2): K_in projected-gradient steps, warm start at x_i."""
+        """Local-Solver (R2): K_in projected-gradient steps, warm start at x_i; or
+        VMLM-B with budget inner_steps + k inner_increment."""
+        if self.prm.local_solver == 1:
+            budget = self.prm.inner_steps + self.k * self.prm.inner_increment
+            x, _ = vmlmb.minimize(lambda w: self.local_value_grad(i, w, ui), xi, h0=self.tau, m=5,
+                                  max_iter=budget)
+            return x
         for _ in range(self.prm.inner_steps):
             xi = np.maximum(0.0, xi - self.tau * self.local_grad(i, xi, ui))
         return xi
@@ -169,6 +191,7 @@ class Deblur:
             else:
                 self.x, self.u = dr_iteration(self.shape, self.windows, self.omegas, self.x, self.u,
                                               self.local_prox, self.prm.rho)
+            self.k += 1
         return self
 
     # ---- diagnostics ------------------------------------------------------
@@ -210,7 +233,8 @@ class Deblur:
 def from_problem(pb, tau: Optional[float] = None, **over) -> Deblur:
     """Build the oracle for a synth.Problem (inputs used verbatim, fp32 -> fp64)."""
     prm = Params(lam=pb.lam, eps=pb.eps, gamma=pb.gamma, rho=pb.rho, reg_kind=pb.reg_kind,
-                 tv_boundary=pb.tv_boundary, inner_steps=pb.inner_steps)
+                 tv_boundary=pb.tv_boundary, inner_steps=pb.inner_steps,
+                 local_solver=getattr(pb, "local_solver", 0), inner_increment=getattr(pb, "inner_increment", 0))
     for k, v in over.items():
         setattr(prm, k, v)
     w = pb.noise_w if pb.noise_w is not None else np.float64(np.float32(pb.noise_w_scalar))
