@@ -142,6 +142,13 @@ typedef struct {
                                      facet solves its own problem, no consensus, no halo exchange,
                                      alpha = 0 (gamma is ignored, also in the default tau);
                                      get_image blends with omega^F.  0: Algorithm 1 (default) */
+    int32_t local_solver;         /* 0: inner_steps projected-gradient steps (R2, default);
+                                     1: VMLM-B (reading V1-V6): projected L-BFGS, m = 5, Armijo
+                                     backtracking, warm start at x_f, budget inner_steps +
+                                     k * inner_increment inner iterations at outer iteration k (P:290:
+                                     10 + 10k); eager launches (host-side line-search decisions); at most
+                                     64 facets per rank */
+    int32_t inner_increment;      /* >= 0, VMLM-B budget increment per outer iteration */
 } deblur_params;
 
 /* 128-byte NCCL unique id for a world > 1 run: call on rank 0, broadcast

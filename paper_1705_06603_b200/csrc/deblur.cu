@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -24,6 +25,7 @@
 #include "fft.hpp"
 #include "kernels.hpp"
 #include "plan.hpp"
+#include "vmlmb.hpp"
 
 using namespace deblur;
 
@@ -99,6 +101,20 @@ struct deblur_ctx {
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     int64_t graph_counts[2][KC_COUNT] = {{0}};
     bool use_graphs = true;
+    // VMLM-B Local-Solver state (local_solver == 1): per local facet gradient pair,
+    // direction, two-loop work vector, free mask and m = 5 memory pairs
+    struct Vm {
+        bool on = false;
+        static constexpr int m = 5;
+        std::vector<float *> G, Gn, D, Q;
+        std::vector<uint8_t *> M;
+        std::vector<std::array<float *, 5>> S, Y;
+        std::vector<std::array<double, 5>> sy, yy;   // <s,y>, <y,y> of each memory slot
+        double *d_part = nullptr;            // [3][ntilesHT]
+        std::vector<double> h_part;
+        int k_outer = 0;                     // outer iteration counter (budget schedule)
+        int64_t evaluations = 0, iterations = 0;
+    } vm;
     // errors
     std::string err;
     bool poisoned = false;
@@ -203,6 +219,8 @@ deblur_status validate(const deblur_params *p, std::string &err) {
     if (p->world > 1 && !p->nccl_id) { err = "nccl_id is NULL with world > 1"; return DEBLUR_EINVAL; }
     if (!(std::isfinite(p->tau))) { err = "tau must be finite"; return DEBLUR_EINVAL; }
     if (p->independent != 0 && p->independent != 1) { err = "independent must be 0 or 1"; return DEBLUR_EINVAL; }
+    if (p->local_solver != 0 && p->local_solver != 1) { err = "local_solver must be 0 (projected gradient) or 1 (VMLM-B)"; return DEBLUR_EINVAL; }
+    if (p->inner_increment < 0) { err = "inner_increment must be >= 0"; return DEBLUR_EINVAL; }
     if (p->operator_mode != DEBLUR_OP_INTERP && p->operator_mode != DEBLUR_OP_PER_NODE) {
         err = "operator_mode must be 0 (interpolated H) or 1 (per-node PSFs)";
         return DEBLUR_EINVAL;
@@ -744,6 +762,33 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
         CUC(cudaMemcpy(h->d_facets_alt, alt.data(), sizeof(FacetDev) * alt.size(), cudaMemcpyHostToDevice));
     }
 
+    // VMLM-B Local-Solver state
+    if (p->local_solver == 1) {
+        if (h->local.size() > (size_t)VM_MAXF) {
+            g_last_error = "VMLM-B Local-Solver: more than 64 facets on one rank";
+            return DEBLUR_EINVAL;
+        }
+        auto &V = h->vm;
+        V.on = true;
+        const size_t nl = h->local.size();
+        V.G.resize(nl); V.Gn.resize(nl); V.D.resize(nl); V.Q.resize(nl); V.M.resize(nl);
+        V.S.resize(nl); V.Y.resize(nl); V.sy.resize(nl); V.yy.resize(nl);
+        for (size_t li = 0; li < nl; ++li) {
+            const size_t ne = (size_t)h->fh[li].ny * h->fh[li].ep;
+            for (float **b : {&V.G[li], &V.Gn[li], &V.D[li], &V.Q[li]}) {
+                CUC(h->dalloc(b, ne));
+                CUC(cudaMemsetAsync(*b, 0, ne * 4, h->stream));
+            }
+            CUC(h->dalloc(&V.M[li], ne));
+            for (int k = 0; k < deblur_ctx::Vm::m; ++k) {
+                CUC(h->dalloc(&V.S[li][k], ne));
+                CUC(h->dalloc(&V.Y[li][k], ne));
+            }
+        }
+        CUC(h->dalloc(&V.d_part, std::max<size_t>(1, 3 * h->tilesHT.size())));
+        V.h_part.resize(3 * h->tilesHT.size() + 1);
+    }
+
     // solver constants
     h->tau = (p->tau > 0) ? p->tau : default_tau(p);
     h->sc.lambda = p->lambda; h->sc.eps = p->eps; h->sc.gamma = p->independent ? 0.f : p->gamma; h->sc.rho = p->rho;
@@ -778,11 +823,245 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
     return DEBLUR_OK;
 }
 
+// ----------------------------------------------------------------- VMLM-B Local-Solver
+// Reading V1-V6 (oracle/vmlmb.py): projected L-BFGS with the free set
+// x > 0 or g < 0, two-loop recursion over the last m = 5 pairs restricted to it,
+// H0 = <s,y>/<y,y> or tau, projected backtracking (Armijo c1 = 1e-4, <= 10 halvings;
+// a facet without an acceptable step stops), pairs kept iff <s,y> > 1e-12 |s||y|.
+// The vector work runs on the device for all local facets at once; the per-facet
+// scalars come back as fp64 partial sums and every decision is taken on the host.
+static VmArgs vm_base(deblur_t h, int nsum) {
+    VmArgs a;
+    std::memset(&a, 0, sizeof a);
+    a.facets = h->d_facets;
+    a.tiles = h->d_tilesHT;
+    a.ntiles = (int)h->tilesHT.size();
+    a.par = h->par;
+    a.nsum = nsum;
+    a.partials = h->vm.d_part;
+    return a;
+}
+
+// per-local-facet sums of the nsum partial rows (tile order; after a stream sync)
+static deblur_status vm_sums(deblur_t h, int nsum, std::vector<std::array<double, 3>> &out) {
+    const size_t nt = h->tilesHT.size();
+    CU(cudaMemcpyAsync(h->vm.h_part.data(), h->vm.d_part, sizeof(double) * 3 * nt, cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    out.assign(h->local.size(), {0.0, 0.0, 0.0});
+    for (int k = 0; k < nsum; ++k)
+        for (size_t t = 0; t < nt; ++t) out[h->tilesHT[t].f][k] += h->vm.h_part[k * nt + t];
+    return DEBLUR_OK;
+}
+
+// f_f(w) + 1/2 |w - u_f|^2_alpha at w = x[par_w] (without the indicator) and its
+// gradient into Gd, for every local facet
+static deblur_status vm_eval(deblur_t h, int par_w, std::vector<float *> &Gd, std::vector<double> &f) {
+    deblur_status s;
+    const size_t nl = h->local.size();
+    std::vector<double> data(nl, 0.0);
+    if (h->conv_path == DEBLUR_CONV_FFT) {
+        if ((s = run_fft_H(h, h->d_facets, par_w, FFT_RESIDUAL)) != DEBLUR_OK) return s;
+        CU(cudaStreamSynchronize(h->stream));
+        CU(fft_data_partials(*h->fft, data));
+        if ((s = run_fft_HT(h, h->d_facets)) != DEBLUR_OK) return s;
+    } else {
+        cudaEvent_t ev = nullptr;
+        h->prof_begin(KC_H, &ev);
+        CU(launch_H_direct(h->conv_args(h->d_facets, false), H_RESIDUAL, par_w, h->stream));
+        h->prof_end(KC_H, ev);
+        CU(cudaMemcpyAsync(h->h_partials.data(), h->d_partials, sizeof(double) * h->tilesH.size(),
+                           cudaMemcpyDeviceToHost, h->stream));
+        CU(cudaStreamSynchronize(h->stream));
+        for (size_t t = 0; t < h->tilesH.size(); ++t) data[h->tilesH[t].f] += h->h_partials[t];
+        ConvArgs ca = h->conv_args(h->d_facets, true);
+        ca.partials = nullptr;
+        h->prof_begin(KC_HT_PLAIN, &ev);
+        CU(launch_HT_direct(ca, HT_PLAIN, par_w, 0, h->sc, h->stream));
+        h->prof_end(KC_HT_PLAIN, ev);
+    }
+    VmArgs a = vm_base(h, 2);
+    a.par = par_w;
+    for (size_t li = 0; li < nl; ++li) a.A[li] = Gd[li];
+    CU(vm_grad(a, h->sc, h->stream));
+    std::vector<std::array<double, 3>> rp;
+    if ((s = vm_sums(h, 2, rp)) != DEBLUR_OK) return s;
+    f.assign(nl, 0.0);
+    for (size_t li = 0; li < nl; ++li) {
+        f[li] = data[li] + (double)h->sc.lambda * rp[li][0] + rp[li][1];
+        if (!std::isfinite(f[li])) {
+            std::ostringstream o;
+            o << "non-finite local objective on facet " << h->local[li] << " (VMLM-B)";
+            return h->fail(DEBLUR_ENUMERIC, o.str());
+        }
+    }
+    ++h->vm.evaluations;
+    return DEBLUR_OK;
+}
+
+static deblur_status vm_local_solve(deblur_t h) {
+    auto &V = h->vm;
+    constexpr int m = deblur_ctx::Vm::m;
+    const size_t nl = h->local.size();
+    const int budget = h->prm.inner_steps + V.k_outer * h->prm.inner_increment;
+    const double h0 = h->tau, c1 = 1e-4;
+    deblur_status s;
+    std::vector<double> f, fn;
+    if ((s = vm_eval(h, h->par, V.G, f)) != DEBLUR_OK) return s;
+    std::vector<int> head(nl, 0), np(nl, 0);
+    std::vector<std::array<double, m>> rho(nl), alpha(nl);
+    std::vector<char> done(nl, 0);
+    std::vector<std::array<double, 3>> sm;
+    for (int it = 0; it < budget; ++it) {
+        if (std::all_of(done.begin(), done.end(), [](char d) { return d != 0; })) break;
+        ++V.iterations;
+        // V2 free set, q = g on it
+        VmArgs a = vm_base(h, 0);
+        for (size_t li = 0; li < nl; ++li) { a.A[li] = V.Q[li]; a.B[li] = V.G[li]; a.Mo[li] = V.M[li]; }
+        CU(vm_mask_q(a, h->stream));
+        // V3 two-loop: newest -> oldest (pair j of facet li: slot (head - 1 - j) mod m)
+        int maxp = 0;
+        for (size_t li = 0; li < nl; ++li) maxp = std::max(maxp, np[li]);
+        auto slot = [&](size_t li, int j) { return ((head[li] - 1 - j) % m + m) % m; };
+        std::vector<std::array<double, 3>> dots;
+        if (maxp > 0) {       // <s_newest, q>
+            VmArgs d = vm_base(h, 1);
+            for (size_t li = 0; li < nl; ++li) { d.B[li] = V.Q[li]; d.C[li] = np[li] > 0 ? V.S[li][slot(li, 0)] : V.Q[li]; }
+            CU(vm_dot(d, h->stream));
+            if ((s = vm_sums(h, 1, dots)) != DEBLUR_OK) return s;
+        }
+        for (int j = 0; j < maxp; ++j) {
+            VmArgs x = vm_base(h, j + 1 < maxp ? 1 : 0);
+            for (size_t li = 0; li < nl; ++li) {
+                const bool has = j < np[li];
+                alpha[li][j] = has ? rho[li][slot(li, j)] * dots[li][0] : 0.0;
+                x.A[li] = V.Q[li];
+                x.B[li] = has ? V.Y[li][slot(li, j)] : nullptr;
+                x.M[li] = V.M[li];
+                x.c0[li] = -alpha[li][j];
+                x.c1[li] = 1.0;
+                x.C[li] = (j + 1 < maxp) ? (j + 1 < np[li] ? V.S[li][slot(li, j + 1)] : V.Q[li]) : nullptr;
+            }
+            CU(vm_axpy_dot(x, h->stream));
+            if (j + 1 < maxp && (s = vm_sums(h, 1, dots)) != DEBLUR_OK) return s;
+        }
+        // r = H0 q (in place in Q), and <y_oldest, r> for the forward loop
+        {
+            VmArgs x = vm_base(h, maxp > 0 ? 1 : 0);
+            for (size_t li = 0; li < nl; ++li) {
+                double H0 = h0;
+                if (np[li] > 0) H0 = V.sy[li][slot(li, 0)] / V.yy[li][slot(li, 0)];
+                x.A[li] = V.Q[li];
+                x.B[li] = nullptr;
+                x.M[li] = V.M[li];
+                x.c0[li] = 0.0;
+                x.c1[li] = H0;
+                x.C[li] = maxp > 0 ? (np[li] > 0 ? V.Y[li][slot(li, np[li] - 1)] : V.Q[li]) : nullptr;
+            }
+            CU(vm_axpy_dot(x, h->stream));
+            if (maxp > 0 && (s = vm_sums(h, 1, dots)) != DEBLUR_OK) return s;
+        }
+        // forward loop oldest -> newest: b = rho <y, r>; r += (alpha - b) s
+        for (int j = maxp - 1; j >= 0; --j) {
+            VmArgs x = vm_base(h, j > 0 ? 1 : 0);
+            for (size_t li = 0; li < nl; ++li) {
+                const bool has = j < np[li];
+                const int jj = has ? j : 0;
+                // the facet's own order: its oldest pair is j = np - 1
+                const bool act = has && j <= np[li] - 1;
+                const double b = act ? rho[li][slot(li, jj)] * dots[li][0] : 0.0;
+                x.A[li] = V.Q[li];
+                x.B[li] = act ? V.S[li][slot(li, jj)] : nullptr;
+                x.M[li] = V.M[li];
+                x.c0[li] = act ? alpha[li][jj] - b : 0.0;
+                x.c1[li] = 1.0;
+                x.C[li] = (j > 0) ? (j - 1 < np[li] ? V.Y[li][slot(li, j - 1)] : V.Q[li]) : nullptr;
+            }
+            CU(vm_axpy_dot(x, h->stream));
+            if (j > 0 && (s = vm_sums(h, 1, dots)) != DEBLUR_OK) return s;
+        }
+        // d = -r on the free set; descent check, else reset (memory dropped, d = -h0 g_F)
+        {
+            VmArgs x = vm_base(h, 1);
+            for (size_t li = 0; li < nl; ++li) {
+                x.A[li] = V.D[li]; x.B[li] = V.Q[li]; x.C[li] = V.G[li]; x.M[li] = V.M[li]; x.c0[li] = 0.0;
+            }
+            CU(vm_direction(x, h->stream));
+            if ((s = vm_sums(h, 1, dots)) != DEBLUR_OK) return s;
+            bool any = false;
+            for (size_t li = 0; li < nl; ++li)
+                if (!(dots[li][0] < 0.0) && !done[li]) { x.c0[li] = h0; np[li] = 0; head[li] = 0; any = true; }
+            if (any) CU(vm_direction(x, h->stream));
+        }
+        // V4 projected backtracking
+        std::vector<double> t(nl, 1.0), gdx(nl, 0.0);
+        std::vector<char> acc(nl, 0);
+        for (size_t li = 0; li < nl; ++li)
+            if (done[li]) { t[li] = 0.0; acc[li] = 1; }
+        bool stalled = false;
+        for (int ls = 0; ls < 10; ++ls) {
+            VmArgs x = vm_base(h, 1);
+            for (size_t li = 0; li < nl; ++li) { x.B[li] = V.D[li]; x.C[li] = V.G[li]; x.c0[li] = t[li]; }
+            CU(vm_trial(x, h->stream));
+            std::vector<std::array<double, 3>> gd;
+            if ((s = vm_sums(h, 1, gd)) != DEBLUR_OK) return s;
+            if ((s = vm_eval(h, h->par ^ 1, V.Gn, fn)) != DEBLUR_OK) return s;
+            bool all = true;
+            for (size_t li = 0; li < nl; ++li) {
+                if (acc[li]) continue;
+                if (fn[li] <= f[li] + c1 * gd[li][0]) acc[li] = 1;
+                else { t[li] *= 0.5; all = false; }
+            }
+            if (all) break;
+            if (ls == 9) stalled = true;
+        }
+        if (stalled) {        // no acceptable step: the facet stops at x (trial with t = 0)
+            for (size_t li = 0; li < nl; ++li)
+                if (!acc[li]) { done[li] = 1; t[li] = 0.0; }
+            VmArgs x = vm_base(h, 1);
+            for (size_t li = 0; li < nl; ++li) { x.B[li] = V.D[li]; x.C[li] = V.G[li]; x.c0[li] = t[li]; }
+            CU(vm_trial(x, h->stream));
+            if ((s = vm_eval(h, h->par ^ 1, V.Gn, fn)) != DEBLUR_OK) return s;
+        }
+        // V5 memory pair
+        {
+            VmArgs x = vm_base(h, 3);
+            for (size_t li = 0; li < nl; ++li) {
+                x.A[li] = V.S[li][head[li]]; x.A2[li] = V.Y[li][head[li]]; x.B[li] = V.G[li]; x.C[li] = V.Gn[li];
+            }
+            CU(vm_pair(x, h->stream));
+            if ((s = vm_sums(h, 3, sm)) != DEBLUR_OK) return s;
+            for (size_t li = 0; li < nl; ++li) {
+                const double sy = sm[li][0], ss = sm[li][1], yy = sm[li][2];
+                if (!done[li] && sy > 1e-12 * std::sqrt(ss) * std::sqrt(yy)) {
+                    rho[li][head[li]] = 1.0 / sy;
+                    V.sy[li][head[li]] = sy;
+                    V.yy[li][head[li]] = yy;
+                    head[li] = (head[li] + 1) % m;
+                    np[li] = std::min(np[li] + 1, m);
+                }
+            }
+        }
+        std::swap(V.G, V.Gn);
+        h->par ^= 1;
+        f = fn;
+    }
+    return DEBLUR_OK;
+}
+
 static deblur_status one_iteration(deblur_t h) {
     deblur_status s;
-    for (int k = 0; k < h->prm.inner_steps; ++k)
-        // independent baseline: no dual / band values either (u stays u0, v unused)
-        if ((s = local_step(h, k == h->prm.inner_steps - 1 && !h->prm.independent)) != DEBLUR_OK) return s;
+    if (h->vm.on) {
+        if ((s = vm_local_solve(h)) != DEBLUR_OK) return s;
+        ++h->vm.k_outer;
+        if (!h->prm.independent) {     // what the last projected-gradient step's epilogue writes
+            VmArgs a = vm_base(h, 0);
+            CU(vm_finalize(a, h->sc.rho, h->stream));
+        }
+    } else {
+        for (int k = 0; k < h->prm.inner_steps; ++k)
+            // independent baseline: no dual / band values either (u stays u0, v unused)
+            if ((s = local_step(h, k == h->prm.inner_steps - 1 && !h->prm.independent)) != DEBLUR_OK) return s;
+    }
     if (h->prm.independent) return DEBLUR_OK;        // baseline: no exchange, no consensus
     if ((s = exchange(h, 0)) != DEBLUR_OK) return s;
     cudaEvent_t ev = nullptr;
@@ -819,7 +1098,7 @@ deblur_status deblur_iterate(deblur_t h, int32_t n) {
     if (s != DEBLUR_OK) return s;
     if (n < 0) return h->fail(DEBLUR_EINVAL, "n must be >= 0");
     int done = 0;
-    if (!h->prof && h->use_graphs && n >= 2) {
+    if (!h->prof && h->use_graphs && n >= 2 && !h->vm.on) {
         const int p0 = h->par;
         if (!h->gexec[p0] && (s = capture_pair(h)) != DEBLUR_OK) return s;
         for (; done + 2 <= n; done += 2) {
@@ -1189,6 +1468,7 @@ deblur_status deblur_reset(deblur_t h, const float *y, const float *x0) {
     if (s != DEBLUR_OK) return s;
     if (!y) return h->fail(DEBLUR_EINVAL, "y is NULL");
     if ((s = upload_y(h, y)) != DEBLUR_OK) return s;
+    h->vm.k_outer = 0;                                // a fresh solve: VMLM-B budget schedule restarts
     return upload_state_x0(h, x0, y);
 }
 

@@ -72,14 +72,12 @@ __device__ __forceinline__ float update_pixel(const FacetDev &F, const float *xh
     return phi;
 }
 
-// Same arithmetic as update_pixel, returning x+ and the dual/band values instead of
-// storing them (the caller vectorises the stores).  Compile-time regulariser / D
-// boundary (REG: 0 smoothed TV, 1 Huber; NEU: Neumann) keep the hot loop branch-free;
-// phi is computed only when asked.
+// TV gradient (D^T psi(D x))(i, j) from the smem halo tile (the divergence form
+// psi_y(i-1,j) - psi_y(i,j) + psi_x(i,j-1) - psi_x(i,j)) and, if asked, phi(D x)(i, j).
+// Compile-time regulariser / D boundary (REG: 0 smoothed TV, 1 Huber; NEU: Neumann).
 template <int REG, bool NEU>
-__device__ __forceinline__ float update_value_t(const FacetDev &F, const float *xh, int XH, int i, int j, int fy,
-                                                int fx, float g, float uc, const SolverConst &sc, bool want_phi,
-                                                float &phi, bool &shared, float &u_new, float &v_new) {
+__device__ __forceinline__ float tv_grad_t(const FacetDev &F, const float *xh, int XH, int i, int j, int fy, int fx,
+                                           const SolverConst &sc, bool want_phi, float &phi) {
     const float e2 = sc.eps * sc.eps;
     auto X = [&](int a, int b) { return xh[a * XH + b]; };
     const float xc = X(i, j);
@@ -114,7 +112,17 @@ __device__ __forceinline__ float update_value_t(const FacetDev &F, const float *
         sc_l = (tl <= d) ? 1.f : d / tl;
         if (want_phi) phi = (tc <= d) ? 0.5f * t2c : d * (tc - 0.5f * d);
     }
-    const float tdiv = dyu * sc_u - dyc * sc_c + dxl * sc_l - dxc * sc_c;
+    return dyu * sc_u - dyc * sc_c + dxl * sc_l - dxc * sc_c;
+}
+
+// Same arithmetic as update_pixel, returning x+ and the dual/band values instead of
+// storing them (the caller vectorises the stores); phi is computed only when asked.
+template <int REG, bool NEU>
+__device__ __forceinline__ float update_value_t(const FacetDev &F, const float *xh, int XH, int i, int j, int fy,
+                                                int fx, float g, float uc, const SolverConst &sc, bool want_phi,
+                                                float &phi, bool &shared, float &u_new, float &v_new) {
+    const float xc = xh[i * XH + j];
+    const float tdiv = tv_grad_t<REG, NEU>(F, xh, XH, i, j, fy, fx, sc, want_phi, phi);
     shared = fy < F.ay.b_prev || fy >= F.ay.b_next || fx < F.ax.b_prev || fx >= F.ax.b_next;
     // A13 ramps are 1 off the bands; per-node weights (F.ay.w) are not
     const float om = (shared || F.ay.w) ? omega_axis(F.ay, fy) * omega_axis(F.ax, fx) : 1.f;

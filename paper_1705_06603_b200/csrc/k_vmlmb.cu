@@ -1,0 +1,239 @@
+// k_vmlmb.cu -- vector kernels of the VMLM-B Local-Solver (PAPER.md:287,
+// :290; reading V1-V6 in DESIGN.md §2 / oracle/vmlmb.py).
+//
+// Every kernel runs over the H^T tile grid (32 x 128 estimate pixels per CTA, all
+// local facets in one launch) and, where a scalar is needed, writes one fp64
+// partial per tile; the host sums a facet's partials in tile order (deterministic,
+// independent of the GPU count) and takes the line-search / memory decisions in
+// fp64.  Per-facet vectors and coefficients arrive by value in VmArgs.
+#include "epilogue.cuh"
+#include "vmlmb.hpp"
+
+namespace deblur {
+namespace {
+
+constexpr int VT_Y = 32, VT_X = 128, VNT = 256, VPT = VT_Y * VT_X / VNT;
+
+__device__ __forceinline__ double block_sum3(double v, double *red, int which) {
+    // one of up to three independent block sums (red holds 3 x 8 doubles)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[which * 8 + (threadIdx.x >> 5)] = v;
+    return v;
+}
+__device__ __forceinline__ void block_finish(double *red, int nsum, double *out, int ntiles) {
+    __syncthreads();
+    if (threadIdx.x < nsum) {
+        double t = 0.0;
+        for (int i = 0; i < VNT / 32; ++i) t += red[threadIdx.x * 8 + i];
+        out[(int64_t)threadIdx.x * ntiles + blockIdx.x] = t;
+    }
+}
+
+// iterate the tile's pixels: fn(local index o, facet row fy, facet col fx)
+template <typename Fn>
+__device__ __forceinline__ void for_tile(const FacetDev &F, const TileDesc &t, Fn fn) {
+#pragma unroll 4
+    for (int i = 0; i < VPT; ++i) {
+        const int idx = threadIdx.x + VNT * i;
+        const int fy = t.y0 + idx / VT_X, fx = t.x0 + idx % VT_X;
+        if (fy < F.ny && fx < F.nx) fn((int64_t)fy * F.ep + fx, fy, fx);
+    }
+}
+
+// M = free set (x > 0 or g < 0) (V2);  A = M ? G : 0  (q of the two-loop)
+__global__ void __launch_bounds__(VNT) k_mask_q(VmArgs a) {
+    const TileDesc t = a.tiles[blockIdx.x];
+    const FacetDev &F = a.facets[t.f];
+    const float *x = F.x[a.par];
+    float *q = a.A[t.f];
+    const float *g = a.B[t.f];
+    uint8_t *m = a.Mo[t.f];
+    for_tile(F, t, [&](int64_t o, int, int) {
+        const bool fr = x[o] > 0.f || g[o] < 0.f;
+        m[o] = fr;
+        q[o] = fr ? g[o] : 0.f;
+    });
+}
+
+// partial <B, C> (and <B, B>, <C, C> when a.nsum == 3)
+__global__ void __launch_bounds__(VNT) k_dot(VmArgs a) {
+    __shared__ double red[3 * 8];
+    const TileDesc t = a.tiles[blockIdx.x];
+    const FacetDev &F = a.facets[t.f];
+    const float *b = a.B[t.f], *c = a.C[t.f];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for_tile(F, t, [&](int64_t o, int, int) {
+        const double bv = b[o], cv = c[o];
+        s0 += bv * cv;
+        s1 += bv * bv;
+        s2 += cv * cv;
+    });
+    block_sum3(s0, red, 0);
+    if (a.nsum > 1) block_sum3(s1, red, 1);
+    if (a.nsum > 2) block_sum3(s2, red, 2);
+    block_finish(red, a.nsum, a.partials, a.ntiles);
+}
+
+// A = c1 * A + c0 * (M ? B : 0);  partial <C, A_new> if C != NULL
+__global__ void __launch_bounds__(VNT) k_axpy_dot(VmArgs a) {
+    __shared__ double red[3 * 8];
+    const TileDesc t = a.tiles[blockIdx.x];
+    const FacetDev &F = a.facets[t.f];
+    float *A = a.A[t.f];
+    const float *B = a.B[t.f], *C = a.C[t.f];
+    const uint8_t *M = a.M[t.f];
+    const float c0 = (float)a.c0[t.f], c1 = (float)a.c1[t.f];
+    double s = 0.0;
+    for_tile(F, t, [&](int64_t o, int, int) {
+        const float bv = (B && M[o]) ? B[o] : 0.f;
+        const float v = c1 * A[o] + c0 * bv;
+        A[o] = v;
+        if (C) s += (double)C[o] * (double)v;
+    });
+    if (a.nsum) {
+        block_sum3(s, red, 0);
+        block_finish(red, 1, a.partials, a.ntiles);
+    }
+}
+
+// direction D = -(M ? A : 0) where c0 == 0, else the reset D = -c0 (M ? G : 0);
+// partial <G, D> (descent check, V3)
+__global__ void __launch_bounds__(VNT) k_direction(VmArgs a) {
+    __shared__ double red[3 * 8];
+    const TileDesc t = a.tiles[blockIdx.x];
+    const FacetDev &F = a.facets[t.f];
+    const float *R = a.B[t.f], *G = a.C[t.f];
+    float *D = a.A[t.f];
+    const uint8_t *M = a.M[t.f];
+    const float h0 = (float)a.c0[t.f];
+    const bool reset = a.c0[t.f] != 0.0;
+    double s = 0.0;
+    for_tile(F, t, [&](int64_t o, int, int) {
+        const float d = M[o] ? (reset ? -h0 * G[o] : -R[o]) : 0.f;
+        D[o] = d;
+        s += (double)G[o] * (double)d;
+    });
+    block_sum3(s, red, 0);
+    block_finish(red, 1, a.partials, a.ntiles);
+}
+
+// trial point x[par^1] = max(0, x[par] + t D) (V1, V4); partial <G, x_t - x>
+__global__ void __launch_bounds__(VNT) k_trial(VmArgs a) {
+    __shared__ double red[3 * 8];
+    const TileDesc t = a.tiles[blockIdx.x];
+    const FacetDev &F = a.facets[t.f];
+    const float *x = F.x[a.par];
+    float *xn = F.x[a.par ^ 1];
+    const float *D = a.B[t.f], *G = a.C[t.f];
+    const float step = (float)a.c0[t.f];
+    double s = 0.0;
+    for_tile(F, t, [&](int64_t o, int, int) {
+        const float v = fmaxf(0.f, x[o] + step * D[o]);
+        xn[o] = v;
+        s += (double)G[o] * ((double)v - (double)x[o]);
+    });
+    block_sum3(s, red, 0);
+    block_finish(red, 1, a.partials, a.ntiles);
+}
+
+// memory pair S = x[par^1] - x[par], Y = Gn - G (V5); partials <s,y>, <s,s>, <y,y>
+__global__ void __launch_bounds__(VNT) k_pair(VmArgs a) {
+    __shared__ double red[3 * 8];
+    const TileDesc t = a.tiles[blockIdx.x];
+    const FacetDev &F = a.facets[t.f];
+    const float *x = F.x[a.par], *xn = F.x[a.par ^ 1];
+    const float *G = a.B[t.f], *Gn = a.C[t.f];
+    float *S = a.A[t.f], *Y = a.A2[t.f];
+    double sy = 0.0, ss = 0.0, yy = 0.0;
+    for_tile(F, t, [&](int64_t o, int, int) {
+        const float s = xn[o] - x[o], y = Gn[o] - G[o];
+        S[o] = s;
+        Y[o] = y;
+        sy += (double)s * y;
+        ss += (double)s * s;
+        yy += (double)y * y;
+    });
+    block_sum3(sy, red, 0);
+    block_sum3(ss, red, 1);
+    block_sum3(yy, red, 2);
+    block_finish(red, 3, a.partials, a.ntiles);
+}
+
+// full local gradient G = g_data + lambda D^T psi(D x) + gamma omega (x - u) at x[par]
+// (g_data = H_f^T W (H_f x - y) already in F.g) and the partials lambda-free
+// sum phi(D x) and 1/2 sum gamma omega (x - u)^2 of the local objective value
+template <int REG, bool NEU>
+__global__ void __launch_bounds__(VNT) k_grad(VmArgs a, SolverConst sc) {
+    constexpr int XH = VT_X + 8;
+    __shared__ __align__(16) float xh[(VT_Y + 2) * XH];
+    __shared__ double red[3 * 8];
+    const TileDesc t = a.tiles[blockIdx.x];
+    const FacetDev &F = a.facets[t.f];
+    const float *__restrict__ x = F.x[a.par];
+    for (int idx = threadIdx.x; idx < (VT_Y + 2) * XH; idx += VNT) {
+        const int i = idx / XH, c = idx - i * XH;
+        int fy = t.y0 - 1 + i, fx = t.x0 - 4 + c;
+        fy = ((fy % F.ny) + F.ny) % F.ny;
+        fx = ((fx % F.nx) + F.nx) % F.nx;
+        xh[idx] = x[(int64_t)fy * F.ep + fx];
+    }
+    __syncthreads();
+    float *G = a.A[t.f];
+    double reg = 0.0, prox = 0.0;
+    for_tile(F, t, [&](int64_t o, int fy, int fx) {
+        const int ly = fy - t.y0, lx = fx - t.x0;
+        float phi;
+        const float tdiv = tv_grad_t<REG, NEU>(F, xh, XH, ly + 1, lx + 4, fy, fx, sc, true, phi);
+        const float xc = xh[(ly + 1) * XH + lx + 4], uc = F.u[o];
+        const bool shared = fy < F.ay.b_prev || fy >= F.ay.b_next || fx < F.ax.b_prev || fx >= F.ax.b_next;
+        const float om = (shared || F.ay.w) ? omega_axis(F.ay, fy) * omega_axis(F.ax, fx) : 1.f;
+        G[o] = F.g[o] + sc.lambda * tdiv + sc.gamma * om * (xc - uc);
+        reg += (double)phi;
+        prox += 0.5 * (double)sc.gamma * (double)om * ((double)xc - uc) * ((double)xc - uc);
+    });
+    block_sum3(reg, red, 0);
+    block_sum3(prox, red, 1);
+    block_finish(red, 2, a.partials, a.ntiles);
+}
+
+// end of the Local-Solver at x[par]: single owners u += rho (x - u); band pixels
+// v = 2x - u (what the last projected-gradient step's epilogue writes)
+__global__ void __launch_bounds__(VNT) k_finalize(VmArgs a, float rho) {
+    const TileDesc t = a.tiles[blockIdx.x];
+    const FacetDev &F = a.facets[t.f];
+    const float *x = F.x[a.par];
+    for_tile(F, t, [&](int64_t o, int fy, int fx) {
+        const bool shared = fy < F.ay.b_prev || fy >= F.ay.b_next || fx < F.ax.b_prev || fx >= F.ax.b_next;
+        const float uc = F.u[o];
+        if (shared) F.v[o] = 2.f * x[o] - uc;
+        else F.u[o] = uc + rho * (x[o] - uc);
+    });
+}
+
+}  // namespace
+
+#define VM_LAUNCH(kern, ...)                                                     \
+    do {                                                                         \
+        if (a.ntiles == 0) return cudaSuccess;                                   \
+        kern<<<a.ntiles, VNT, 0, s>>>(__VA_ARGS__);                              \
+        return cudaGetLastError();                                               \
+    } while (0)
+
+cudaError_t vm_mask_q(const VmArgs &a, cudaStream_t s) { VM_LAUNCH(k_mask_q, a); }
+cudaError_t vm_dot(const VmArgs &a, cudaStream_t s) { VM_LAUNCH(k_dot, a); }
+cudaError_t vm_axpy_dot(const VmArgs &a, cudaStream_t s) { VM_LAUNCH(k_axpy_dot, a); }
+cudaError_t vm_direction(const VmArgs &a, cudaStream_t s) { VM_LAUNCH(k_direction, a); }
+cudaError_t vm_trial(const VmArgs &a, cudaStream_t s) { VM_LAUNCH(k_trial, a); }
+cudaError_t vm_pair(const VmArgs &a, cudaStream_t s) { VM_LAUNCH(k_pair, a); }
+cudaError_t vm_finalize(const VmArgs &a, float rho, cudaStream_t s) { VM_LAUNCH(k_finalize, a, rho); }
+cudaError_t vm_grad(const VmArgs &a, const SolverConst &sc, cudaStream_t s) {
+    if (a.ntiles == 0) return cudaSuccess;
+    if (sc.reg_kind == 0 && sc.tv_boundary == 0) k_grad<0, false><<<a.ntiles, VNT, 0, s>>>(a, sc);
+    else if (sc.reg_kind == 0) k_grad<0, true><<<a.ntiles, VNT, 0, s>>>(a, sc);
+    else if (sc.tv_boundary == 0) k_grad<1, false><<<a.ntiles, VNT, 0, s>>>(a, sc);
+    else k_grad<1, true><<<a.ntiles, VNT, 0, s>>>(a, sc);
+    return cudaGetLastError();
+}
+
+}  // namespace deblur

@@ -45,6 +45,7 @@ class Params(ctypes.Structure):
         ("nccl_id", ctypes.c_void_p),
         ("operator_mode", ctypes.c_int32),
         ("independent", ctypes.c_int32),
+        ("local_solver", ctypes.c_int32), ("inner_increment", ctypes.c_int32),
     ]
 
 
@@ -136,7 +137,8 @@ def make_params(psfs, wy, wx, y, noise_w=None, noise_w_scalar: float = 1.0, lam:
                 eps: float = 1e-3, reg_kind: int = 0, tv_boundary: int = 0, gamma: float = 0.0, rho: float = 1.0,
                 tau: float = 0.0, inner_steps: int = 1, facet_gy: int = 1, facet_gx: int = 1, overlap: int = 0,
                 x0=None, conv_path: int = CONV_AUTO, rank: int = 0, world: int = 1, device: int = 0,
-                nccl_id_bytes: Optional[bytes] = None, operator_mode: int = 0, independent: int = 0):
+                nccl_id_bytes: Optional[bytes] = None, operator_mode: int = 0, independent: int = 0,
+                local_solver: int = 0, inner_increment: int = 0):
     """Returns (Params, keepalive) -- keepalive holds the arrays the pointers refer to."""
     psfs = _f32(psfs)
     wy, wx, y = _f32(wy), _f32(wx), _f32(y)
@@ -162,7 +164,8 @@ def make_params(psfs, wy, wx, y, noise_w=None, noise_w_scalar: float = 1.0, lam:
                gamma=gamma, rho=rho, tau=tau, inner_steps=inner_steps, facet_gy=facet_gy, facet_gx=facet_gx,
                overlap=overlap, x0=_ptr(x0a), conv_path=conv_path, rank=rank, world=world, device=device,
                nccl_id=ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None,
-               operator_mode=operator_mode, independent=int(independent))
+               operator_mode=operator_mode, independent=int(independent), local_solver=local_solver,
+               inner_increment=inner_increment)
     return p, keep
 
 
@@ -171,7 +174,8 @@ def problem_params(pb, **over):
     kw = dict(noise_w=pb.noise_w, noise_w_scalar=pb.noise_w_scalar, lam=pb.lam, eps=pb.eps,
               reg_kind=pb.reg_kind, tv_boundary=pb.tv_boundary, gamma=pb.gamma, rho=pb.rho,
               inner_steps=pb.inner_steps, facet_gy=pb.fy, facet_gx=pb.fx, overlap=pb.overlap, x0=pb.x0,
-              operator_mode=getattr(pb, "operator_mode", 0), independent=getattr(pb, "independent", 0))
+              operator_mode=getattr(pb, "operator_mode", 0), independent=getattr(pb, "independent", 0),
+              local_solver=getattr(pb, "local_solver", 0), inner_increment=getattr(pb, "inner_increment", 0))
     kw.update(over)
     return make_params(pb.psfs, pb.wy, pb.wx, pb.y, **kw)
 

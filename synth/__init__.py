@@ -64,6 +64,8 @@ class Problem:
     x0: Optional[np.ndarray] = None
     operator_mode: int = 0    # 0: interpolated H restricted to facets; 1: per-node PSFs
     independent: int = 0      # 1: the paper's independent baseline (no consensus, alpha = 0)
+    local_solver: int = 0     # 0: projected gradient (inner_steps); 1: VMLM-B (budget inner_steps + k inner_increment)
+    inner_increment: int = 0
 
     @property
     def my(self) -> int:
