@@ -112,6 +112,8 @@ def run_ours(args, rank, world, local):
     pb = synth.make_config(args.config)
     if args.operator_mode == 1:
         pb = synth.per_node(pb)
+    if args.local_solver == "vmlmb":
+        pb.local_solver, pb.inner_steps, pb.inner_increment = 1, args.inner, args.inner_inc
     nid = None
     if world > 1:
         import torch.distributed as dist
@@ -243,6 +245,7 @@ def run_ours(args, rank, world, local):
             "config": {"workload": f"c{args.config}", "image": f"{pb.ny}x{pb.nx}", "psf": f"{pb.P}x{pb.P}",
                        "psf_grid": f"{pb.gy}x{pb.gx}", "facets": f"{pb.fy}x{pb.fx}", "overlap": pb.overlap,
                        "lambda": pb.lam, "eps": pb.eps, "iterations_per_step": 1, "inner_steps": pb.inner_steps,
+                       "local_solver": {0: "projected gradient", 1: "VMLM-B"}[pb.local_solver],
                        "conv_path": {1: "direct", 2: "fft"}[dev.conv_path],
                        "operator_mode": {0: "interpolated H per facet", 1: "per-node PSFs (paper node model)"}[
                            args.operator_mode],
@@ -329,6 +332,10 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--path", choices=["auto", "direct", "fft"], default="auto")
+    ap.add_argument("--local-solver", choices=["pg", "vmlmb"], default="pg",
+                    help="pg: one projected-gradient step per iteration (north star); vmlmb: VMLM-B inner solves")
+    ap.add_argument("--inner", type=int, default=10, help="VMLM-B inner budget at the first outer iteration")
+    ap.add_argument("--inner-inc", type=int, default=0, help="VMLM-B budget increment per outer iteration")
     ap.add_argument("--operator-mode", type=int, choices=[0, 1], default=0,
                     help="0: interpolated H restricted to facets (north star); 1: per-node PSFs, facets = PSF grid")
     ap.add_argument("--no-cpu", action="store_true")

@@ -35,12 +35,12 @@ thread_local std::string g_last_error;
 
 enum KClass {
     KC_H = 0, KC_HT_UPDATE, KC_CONSENSUS, KC_H_OBJ, KC_TV, KC_MAXDIFF, KC_XCHG, KC_HT_PLAIN, KC_H_PLAIN,
-    KC_FFT_H0, KC_FFT_H1, KC_FFT_H2, KC_FFT_HT0, KC_FFT_HT1, KC_FFT_HT2, KC_UPDATE_G, KC_COUNT
+    KC_FFT_H0, KC_FFT_H1, KC_FFT_H2, KC_FFT_HT0, KC_FFT_HT1, KC_FFT_HT2, KC_UPDATE_G, KC_VM_VEC, KC_VM_GRAD, KC_COUNT
 };
 const char *k_names[KC_COUNT] = {"H_direct_residual", "HT_direct_update", "consensus", "H_direct_objective",
                                  "tv_value", "maxdiff", "halo_exchange", "HT_direct_plain", "H_direct_plain",
                                  "H_fft_rows", "H_fft_cols", "H_fft_rows_inv", "HT_fft_rows", "HT_fft_cols",
-                                 "HT_fft_rows_inv", "update_from_g"};
+                                 "HT_fft_rows_inv", "update_from_g", "vmlmb_vector", "vmlmb_grad"};
 
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
@@ -830,6 +830,14 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
 // a facet without an acceptable step stops), pairs kept iff <s,y> > 1e-12 |s||y|.
 // The vector work runs on the device for all local facets at once; the per-facet
 // scalars come back as fp64 partial sums and every decision is taken on the host.
+#define VMK(cls, call)                          \
+    do {                                        \
+        cudaEvent_t ev_ = nullptr;              \
+        h->prof_begin(cls, &ev_);               \
+        CU(call);                               \
+        h->prof_end(cls, ev_);                  \
+    } while (0)
+
 static VmArgs vm_base(deblur_t h, int nsum) {
     VmArgs a;
     std::memset(&a, 0, sizeof a);
@@ -882,7 +890,7 @@ static deblur_status vm_eval(deblur_t h, int par_w, std::vector<float *> &Gd, st
     VmArgs a = vm_base(h, 2);
     a.par = par_w;
     for (size_t li = 0; li < nl; ++li) a.A[li] = Gd[li];
-    CU(vm_grad(a, h->sc, h->stream));
+    VMK(KC_VM_GRAD, vm_grad(a, h->sc, h->stream));
     std::vector<std::array<double, 3>> rp;
     if ((s = vm_sums(h, 2, rp)) != DEBLUR_OK) return s;
     f.assign(nl, 0.0);
@@ -917,7 +925,7 @@ static deblur_status vm_local_solve(deblur_t h) {
         // V2 free set, q = g on it
         VmArgs a = vm_base(h, 0);
         for (size_t li = 0; li < nl; ++li) { a.A[li] = V.Q[li]; a.B[li] = V.G[li]; a.Mo[li] = V.M[li]; }
-        CU(vm_mask_q(a, h->stream));
+        VMK(KC_VM_VEC, vm_mask_q(a, h->stream));
         // V3 two-loop: newest -> oldest (pair j of facet li: slot (head - 1 - j) mod m)
         int maxp = 0;
         for (size_t li = 0; li < nl; ++li) maxp = std::max(maxp, np[li]);
@@ -926,7 +934,7 @@ static deblur_status vm_local_solve(deblur_t h) {
         if (maxp > 0) {       // <s_newest, q>
             VmArgs d = vm_base(h, 1);
             for (size_t li = 0; li < nl; ++li) { d.B[li] = V.Q[li]; d.C[li] = np[li] > 0 ? V.S[li][slot(li, 0)] : V.Q[li]; }
-            CU(vm_dot(d, h->stream));
+            VMK(KC_VM_VEC, vm_dot(d, h->stream));
             if ((s = vm_sums(h, 1, dots)) != DEBLUR_OK) return s;
         }
         for (int j = 0; j < maxp; ++j) {
@@ -941,7 +949,7 @@ static deblur_status vm_local_solve(deblur_t h) {
                 x.c1[li] = 1.0;
                 x.C[li] = (j + 1 < maxp) ? (j + 1 < np[li] ? V.S[li][slot(li, j + 1)] : V.Q[li]) : nullptr;
             }
-            CU(vm_axpy_dot(x, h->stream));
+            VMK(KC_VM_VEC, vm_axpy_dot(x, h->stream));
             if (j + 1 < maxp && (s = vm_sums(h, 1, dots)) != DEBLUR_OK) return s;
         }
         // r = H0 q (in place in Q), and <y_oldest, r> for the forward loop
@@ -957,7 +965,7 @@ static deblur_status vm_local_solve(deblur_t h) {
                 x.c1[li] = H0;
                 x.C[li] = maxp > 0 ? (np[li] > 0 ? V.Y[li][slot(li, np[li] - 1)] : V.Q[li]) : nullptr;
             }
-            CU(vm_axpy_dot(x, h->stream));
+            VMK(KC_VM_VEC, vm_axpy_dot(x, h->stream));
             if (maxp > 0 && (s = vm_sums(h, 1, dots)) != DEBLUR_OK) return s;
         }
         // forward loop oldest -> newest: b = rho <y, r>; r += (alpha - b) s
@@ -976,7 +984,7 @@ static deblur_status vm_local_solve(deblur_t h) {
                 x.c1[li] = 1.0;
                 x.C[li] = (j > 0) ? (j - 1 < np[li] ? V.Y[li][slot(li, j - 1)] : V.Q[li]) : nullptr;
             }
-            CU(vm_axpy_dot(x, h->stream));
+            VMK(KC_VM_VEC, vm_axpy_dot(x, h->stream));
             if (j > 0 && (s = vm_sums(h, 1, dots)) != DEBLUR_OK) return s;
         }
         // d = -r on the free set; descent check, else reset (memory dropped, d = -h0 g_F)
@@ -985,12 +993,12 @@ static deblur_status vm_local_solve(deblur_t h) {
             for (size_t li = 0; li < nl; ++li) {
                 x.A[li] = V.D[li]; x.B[li] = V.Q[li]; x.C[li] = V.G[li]; x.M[li] = V.M[li]; x.c0[li] = 0.0;
             }
-            CU(vm_direction(x, h->stream));
+            VMK(KC_VM_VEC, vm_direction(x, h->stream));
             if ((s = vm_sums(h, 1, dots)) != DEBLUR_OK) return s;
             bool any = false;
             for (size_t li = 0; li < nl; ++li)
                 if (!(dots[li][0] < 0.0) && !done[li]) { x.c0[li] = h0; np[li] = 0; head[li] = 0; any = true; }
-            if (any) CU(vm_direction(x, h->stream));
+            if (any) VMK(KC_VM_VEC, vm_direction(x, h->stream));
         }
         // V4 projected backtracking
         std::vector<double> t(nl, 1.0), gdx(nl, 0.0);
@@ -1001,7 +1009,7 @@ static deblur_status vm_local_solve(deblur_t h) {
         for (int ls = 0; ls < 10; ++ls) {
             VmArgs x = vm_base(h, 1);
             for (size_t li = 0; li < nl; ++li) { x.B[li] = V.D[li]; x.C[li] = V.G[li]; x.c0[li] = t[li]; }
-            CU(vm_trial(x, h->stream));
+            VMK(KC_VM_VEC, vm_trial(x, h->stream));
             std::vector<std::array<double, 3>> gd;
             if ((s = vm_sums(h, 1, gd)) != DEBLUR_OK) return s;
             if ((s = vm_eval(h, h->par ^ 1, V.Gn, fn)) != DEBLUR_OK) return s;
@@ -1019,7 +1027,7 @@ static deblur_status vm_local_solve(deblur_t h) {
                 if (!acc[li]) { done[li] = 1; t[li] = 0.0; }
             VmArgs x = vm_base(h, 1);
             for (size_t li = 0; li < nl; ++li) { x.B[li] = V.D[li]; x.C[li] = V.G[li]; x.c0[li] = t[li]; }
-            CU(vm_trial(x, h->stream));
+            VMK(KC_VM_VEC, vm_trial(x, h->stream));
             if ((s = vm_eval(h, h->par ^ 1, V.Gn, fn)) != DEBLUR_OK) return s;
         }
         // V5 memory pair
@@ -1028,7 +1036,7 @@ static deblur_status vm_local_solve(deblur_t h) {
             for (size_t li = 0; li < nl; ++li) {
                 x.A[li] = V.S[li][head[li]]; x.A2[li] = V.Y[li][head[li]]; x.B[li] = V.G[li]; x.C[li] = V.Gn[li];
             }
-            CU(vm_pair(x, h->stream));
+            VMK(KC_VM_VEC, vm_pair(x, h->stream));
             if ((s = vm_sums(h, 3, sm)) != DEBLUR_OK) return s;
             for (size_t li = 0; li < nl; ++li) {
                 const double sy = sm[li][0], ss = sm[li][1], yy = sm[li][2];
@@ -1055,7 +1063,7 @@ static deblur_status one_iteration(deblur_t h) {
         ++h->vm.k_outer;
         if (!h->prm.independent) {     // what the last projected-gradient step's epilogue writes
             VmArgs a = vm_base(h, 0);
-            CU(vm_finalize(a, h->sc.rho, h->stream));
+            VMK(KC_VM_VEC, vm_finalize(a, h->sc.rho, h->stream));
         }
     } else {
         for (int k = 0; k < h->prm.inner_steps; ++k)
