@@ -30,14 +30,43 @@ __device__ __forceinline__ void block_finish(double *red, int nsum, double *out,
     }
 }
 
-// iterate the tile's pixels: fn(local index o, facet row fy, facet col fx)
+// iterate the tile in groups of 4 consecutive pixels of a row (a warp covers one
+// 128-pixel row: 512-byte coalesced accesses, 16-byte vectors when the group is
+// whole): fn(offset o of the first pixel, facet row fy, facet col fx, count nv)
 template <typename Fn>
-__device__ __forceinline__ void for_tile(const FacetDev &F, const TileDesc &t, Fn fn) {
-#pragma unroll 4
-    for (int i = 0; i < VPT; ++i) {
-        const int idx = threadIdx.x + VNT * i;
-        const int fy = t.y0 + idx / VT_X, fx = t.x0 + idx % VT_X;
-        if (fy < F.ny && fx < F.nx) fn((int64_t)fy * F.ep + fx, fy, fx);
+__device__ __forceinline__ void for_tile4(const FacetDev &F, const TileDesc &t, Fn fn) {
+#pragma unroll
+    for (int i = 0; i < VT_Y * VT_X / 4 / VNT; ++i) {
+        const int gi = threadIdx.x + VNT * i;
+        const int fy = t.y0 + (gi >> 5), fx = t.x0 + 4 * (gi & 31);
+        if (fy < F.ny && fx < F.nx) fn((int64_t)fy * F.ep + fx, fy, fx, min(4, F.nx - fx));
+    }
+}
+__device__ __forceinline__ void ld4(const float *p, int nv, float (&v)[4]) {
+    if (nv == 4) {
+        const float4 q = *reinterpret_cast<const float4 *>(p);
+        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = j < nv ? p[j] : 0.f;
+    }
+}
+__device__ __forceinline__ void st4(float *p, int nv, const float (&v)[4]) {
+    if (nv == 4) {
+        *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (j < nv) p[j] = v[j];
+    }
+}
+__device__ __forceinline__ void ldm4(const uint8_t *p, int nv, bool (&m)[4]) {
+    if (nv == 4) {
+        const uchar4 q = *reinterpret_cast<const uchar4 *>(p);
+        m[0] = q.x; m[1] = q.y; m[2] = q.z; m[3] = q.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) m[j] = j < nv ? p[j] != 0 : false;
     }
 }
 
@@ -49,10 +78,21 @@ __global__ void __launch_bounds__(VNT) k_mask_q(VmArgs a) {
     float *q = a.A[t.f];
     const float *g = a.B[t.f];
     uint8_t *m = a.Mo[t.f];
-    for_tile(F, t, [&](int64_t o, int, int) {
-        const bool fr = x[o] > 0.f || g[o] < 0.f;
-        m[o] = fr;
-        q[o] = fr ? g[o] : 0.f;
+    for_tile4(F, t, [&](int64_t o, int, int, int nv) {
+        float xv[4], gv[4], qv[4];
+        ld4(x + o, nv, xv);
+        ld4(g + o, nv, gv);
+        uchar4 mv;
+        bool fr[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            fr[j] = xv[j] > 0.f || gv[j] < 0.f;
+            qv[j] = fr[j] ? gv[j] : 0.f;
+        }
+        mv = make_uchar4(fr[0], fr[1], fr[2], fr[3]);
+        if (nv == 4) *reinterpret_cast<uchar4 *>(m + o) = mv;
+        else for (int j = 0; j < nv; ++j) m[o + j] = fr[j];
+        st4(q + o, nv, qv);
     });
 }
 
@@ -63,11 +103,16 @@ __global__ void __launch_bounds__(VNT) k_dot(VmArgs a) {
     const FacetDev &F = a.facets[t.f];
     const float *b = a.B[t.f], *c = a.C[t.f];
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-    for_tile(F, t, [&](int64_t o, int, int) {
-        const double bv = b[o], cv = c[o];
-        s0 += bv * cv;
-        s1 += bv * bv;
-        s2 += cv * cv;
+    for_tile4(F, t, [&](int64_t o, int, int, int nv) {
+        float bv[4], cv[4];
+        ld4(b + o, nv, bv);
+        ld4(c + o, nv, cv);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            s0 += (double)bv[j] * cv[j];
+            s1 += (double)bv[j] * bv[j];
+            s2 += (double)cv[j] * cv[j];
+        }
     });
     block_sum3(s0, red, 0);
     if (a.nsum > 1) block_sum3(s1, red, 1);
@@ -85,11 +130,24 @@ __global__ void __launch_bounds__(VNT) k_axpy_dot(VmArgs a) {
     const uint8_t *M = a.M[t.f];
     const float c0 = (float)a.c0[t.f], c1 = (float)a.c1[t.f];
     double s = 0.0;
-    for_tile(F, t, [&](int64_t o, int, int) {
-        const float bv = (B && M[o]) ? B[o] : 0.f;
-        const float v = c1 * A[o] + c0 * bv;
-        A[o] = v;
-        if (C) s += (double)C[o] * (double)v;
+    for_tile4(F, t, [&](int64_t o, int, int, int nv) {
+        float av[4], bv[4] = {0.f, 0.f, 0.f, 0.f}, cv[4];
+        bool mv[4];
+        ld4(A + o, nv, av);
+        if (B) {
+            ld4(B + o, nv, bv);
+            ldm4(M + o, nv, mv);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bv[j] = mv[j] ? bv[j] : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) av[j] = c1 * av[j] + c0 * bv[j];
+        st4(A + o, nv, av);
+        if (C) {
+            ld4(C + o, nv, cv);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) s += (double)cv[j] * (double)av[j];
+        }
     });
     if (a.nsum) {
         block_sum3(s, red, 0);
@@ -97,7 +155,7 @@ __global__ void __launch_bounds__(VNT) k_axpy_dot(VmArgs a) {
     }
 }
 
-// direction D = -(M ? A : 0) where c0 == 0, else the reset D = -c0 (M ? G : 0);
+// direction D = -(M ? R : 0) where c0 == 0, else the reset D = -c0 (M ? G : 0);
 // partial <G, D> (descent check, V3)
 __global__ void __launch_bounds__(VNT) k_direction(VmArgs a) {
     __shared__ double red[3 * 8];
@@ -109,10 +167,18 @@ __global__ void __launch_bounds__(VNT) k_direction(VmArgs a) {
     const float h0 = (float)a.c0[t.f];
     const bool reset = a.c0[t.f] != 0.0;
     double s = 0.0;
-    for_tile(F, t, [&](int64_t o, int, int) {
-        const float d = M[o] ? (reset ? -h0 * G[o] : -R[o]) : 0.f;
-        D[o] = d;
-        s += (double)G[o] * (double)d;
+    for_tile4(F, t, [&](int64_t o, int, int, int nv) {
+        float rv[4], gv[4], dv[4];
+        bool mv[4];
+        ld4(R + o, nv, rv);
+        ld4(G + o, nv, gv);
+        ldm4(M + o, nv, mv);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            dv[j] = mv[j] ? (reset ? -h0 * gv[j] : -rv[j]) : 0.f;
+            s += (double)gv[j] * (double)dv[j];
+        }
+        st4(D + o, nv, dv);
     });
     block_sum3(s, red, 0);
     block_finish(red, 1, a.partials, a.ntiles);
@@ -128,10 +194,17 @@ __global__ void __launch_bounds__(VNT) k_trial(VmArgs a) {
     const float *D = a.B[t.f], *G = a.C[t.f];
     const float step = (float)a.c0[t.f];
     double s = 0.0;
-    for_tile(F, t, [&](int64_t o, int, int) {
-        const float v = fmaxf(0.f, x[o] + step * D[o]);
-        xn[o] = v;
-        s += (double)G[o] * ((double)v - (double)x[o]);
+    for_tile4(F, t, [&](int64_t o, int, int, int nv) {
+        float xv[4], dv[4], gv[4], nvv[4];
+        ld4(x + o, nv, xv);
+        ld4(D + o, nv, dv);
+        ld4(G + o, nv, gv);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            nvv[j] = fmaxf(0.f, xv[j] + step * dv[j]);
+            s += (double)gv[j] * ((double)nvv[j] - (double)xv[j]);
+        }
+        st4(xn + o, nv, nvv);
     });
     block_sum3(s, red, 0);
     block_finish(red, 1, a.partials, a.ntiles);
@@ -146,13 +219,22 @@ __global__ void __launch_bounds__(VNT) k_pair(VmArgs a) {
     const float *G = a.B[t.f], *Gn = a.C[t.f];
     float *S = a.A[t.f], *Y = a.A2[t.f];
     double sy = 0.0, ss = 0.0, yy = 0.0;
-    for_tile(F, t, [&](int64_t o, int, int) {
-        const float s = xn[o] - x[o], y = Gn[o] - G[o];
-        S[o] = s;
-        Y[o] = y;
-        sy += (double)s * y;
-        ss += (double)s * s;
-        yy += (double)y * y;
+    for_tile4(F, t, [&](int64_t o, int, int, int nv) {
+        float xv[4], xnv[4], gv[4], gnv[4], sv[4], yv[4];
+        ld4(x + o, nv, xv);
+        ld4(xn + o, nv, xnv);
+        ld4(G + o, nv, gv);
+        ld4(Gn + o, nv, gnv);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            sv[j] = xnv[j] - xv[j];
+            yv[j] = gnv[j] - gv[j];
+            sy += (double)sv[j] * yv[j];
+            ss += (double)sv[j] * sv[j];
+            yy += (double)yv[j] * yv[j];
+        }
+        st4(S + o, nv, sv);
+        st4(Y + o, nv, yv);
     });
     block_sum3(sy, red, 0);
     block_sum3(ss, red, 1);
@@ -171,17 +253,40 @@ __global__ void __launch_bounds__(VNT) k_grad(VmArgs a, SolverConst sc) {
     const TileDesc t = a.tiles[blockIdx.x];
     const FacetDev &F = a.facets[t.f];
     const float *__restrict__ x = F.x[a.par];
-    for (int idx = threadIdx.x; idx < (VT_Y + 2) * XH; idx += VNT) {
-        const int i = idx / XH, c = idx - i * XH;
-        int fy = t.y0 - 1 + i, fx = t.x0 - 4 + c;
-        fy = ((fy % F.ny) + F.ny) % F.ny;
-        fx = ((fx % F.nx) + F.nx) % F.nx;
-        xh[idx] = x[(int64_t)fy * F.ep + fx];
+    const bool interior = t.y0 >= 1 && t.y0 + VT_Y + 1 <= F.ny && t.x0 >= 4 && t.x0 + VT_X + 4 <= F.nx;
+    if (interior) {            // 16-byte loads, all in flight (row starts x0 - 4: 16-byte aligned)
+        constexpr int NV = XH / 4;
+        constexpr int PER = ((VT_Y + 2) * NV + VNT - 1) / VNT;
+        float4 tmp[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int idx = threadIdx.x + VNT * k;
+            if (idx < (VT_Y + 2) * NV) {
+                const int i = idx / NV, v = idx - i * NV;
+                tmp[k] = __ldg(reinterpret_cast<const float4 *>(x + (int64_t)(t.y0 - 1 + i) * F.ep + t.x0 - 4) + v);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int idx = threadIdx.x + VNT * k;
+            if (idx < (VT_Y + 2) * NV) *reinterpret_cast<float4 *>(xh + 4 * idx) = tmp[k];
+        }
+    } else {
+        for (int idx = threadIdx.x; idx < (VT_Y + 2) * XH; idx += VNT) {
+            const int i = idx / XH, c = idx - i * XH;
+            int fy = t.y0 - 1 + i, fx = t.x0 - 4 + c;
+            fy = ((fy % F.ny) + F.ny) % F.ny;
+            fx = ((fx % F.nx) + F.nx) % F.nx;
+            xh[idx] = x[(int64_t)fy * F.ep + fx];
+        }
     }
     __syncthreads();
     float *G = a.A[t.f];
     double reg = 0.0, prox = 0.0;
-    for_tile(F, t, [&](int64_t o, int fy, int fx) {
+    for_tile4(F, t, [&](int64_t o4, int fy, int fx4, int nv) {
+      for (int jj = 0; jj < nv; ++jj) {
+        const int fx = fx4 + jj;
+        const int64_t o = o4 + jj;
         const int ly = fy - t.y0, lx = fx - t.x0;
         float phi;
         const float tdiv = tv_grad_t<REG, NEU>(F, xh, XH, ly + 1, lx + 4, fy, fx, sc, true, phi);
@@ -191,6 +296,7 @@ __global__ void __launch_bounds__(VNT) k_grad(VmArgs a, SolverConst sc) {
         G[o] = F.g[o] + sc.lambda * tdiv + sc.gamma * om * (xc - uc);
         reg += (double)phi;
         prox += 0.5 * (double)sc.gamma * (double)om * ((double)xc - uc) * ((double)xc - uc);
+      }
     });
     block_sum3(reg, red, 0);
     block_sum3(prox, red, 1);
@@ -203,11 +309,15 @@ __global__ void __launch_bounds__(VNT) k_finalize(VmArgs a, float rho) {
     const TileDesc t = a.tiles[blockIdx.x];
     const FacetDev &F = a.facets[t.f];
     const float *x = F.x[a.par];
-    for_tile(F, t, [&](int64_t o, int fy, int fx) {
-        const bool shared = fy < F.ay.b_prev || fy >= F.ay.b_next || fx < F.ax.b_prev || fx >= F.ax.b_next;
-        const float uc = F.u[o];
-        if (shared) F.v[o] = 2.f * x[o] - uc;
-        else F.u[o] = uc + rho * (x[o] - uc);
+    for_tile4(F, t, [&](int64_t o4, int fy, int fx4, int nv) {
+        for (int jj = 0; jj < nv; ++jj) {
+            const int fx = fx4 + jj;
+            const int64_t o = o4 + jj;
+            const bool shared = fy < F.ay.b_prev || fy >= F.ay.b_next || fx < F.ax.b_prev || fx >= F.ax.b_next;
+            const float uc = F.u[o];
+            if (shared) F.v[o] = 2.f * x[o] - uc;
+            else F.u[o] = uc + rho * (x[o] - uc);
+        }
     });
 }
 
