@@ -35,8 +35,11 @@
 #ifndef COLS_TMEM
 #define COLS_TMEM 1
 #endif
+#ifndef COLS_TM_NB
+#define COLS_TM_NB 8
+#endif
 #ifndef COLS_TM_MINB
-#define COLS_TM_MINB 2
+#define COLS_TM_MINB (16 / COLS_TM_NB)
 #endif
 
 namespace deblur {
@@ -292,7 +295,7 @@ template <int S>
 struct GC {
     // 256 threads, 8 columns per CTA from S = 256 up: ~104 KB smem at S = 512, two CTAs per SM
     static constexpr int NTH = (S <= 128) ? 512 : 256;
-    static constexpr int NB = (S <= 64) ? 64 : (S <= 128) ? 32 : 8;
+    static constexpr int NB = (S <= 64) ? 64 : (S <= 128) ? 32 : (S == 512 && COLS_TMEM) ? COLS_TM_NB : 8;
     static constexpr int CS = S + ((NB >= 16) ? 1 : 16 / NB);
     using F = Fft<S, NB, CS, NTH>;
     static constexpr int E = F::E;
@@ -740,9 +743,11 @@ __device__ __forceinline__ void tm_get(uint32_t ta, float2 (&v)[E]) {
 
 template <int S>
 struct GCT {
-    static constexpr int NTH = 256, NB = 8, CS = S + 2;
+    // NB columns per CTA with NTH = 32 NB threads: 16 elements per thread at S = 512;
+    // CS = S + 16/NB makes the paired 16-byte exchanges conflict-free per quarter-warp
+    static constexpr int NB = COLS_TM_NB, NTH = 32 * NB, CS = S + 16 / NB;
     static constexpr int E = NB * S / NTH;
-    static constexpr int TMCOLS = 128;      // per CTA: 4 lane quarters x (2 warps x 64 columns)
+    static constexpr int TMCOLS = NB >= 8 ? 64 * (NB / 4) : 64;   // 4 lane quarters x (NB/4 warps x 64 columns)
     using F = Fft<S, NB, CS, NTH>;
 };
 template <int S>
@@ -753,7 +758,7 @@ static size_t smem_cols_tm(int NP, int NQ) {
 }
 
 template <int S>
-__global__ void __launch_bounds__(256, COLS_TM_MINB) k_cols_tm(FftArgs A, int mode) {
+__global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftArgs A, int mode) {
     using G = GCT<S>;
     using F = typename G::F;
     using S0 = typename F::First;
