@@ -35,12 +35,15 @@ thread_local std::string g_last_error;
 
 enum KClass {
     KC_H = 0, KC_HT_UPDATE, KC_CONSENSUS, KC_H_OBJ, KC_TV, KC_MAXDIFF, KC_XCHG, KC_HT_PLAIN, KC_H_PLAIN,
-    KC_FFT_H0, KC_FFT_H1, KC_FFT_H2, KC_FFT_HT0, KC_FFT_HT1, KC_FFT_HT2, KC_UPDATE_G, KC_VM_VEC, KC_VM_GRAD, KC_COUNT
+    KC_FFT_H0, KC_FFT_H1, KC_FFT_H2, KC_FFT_HT0, KC_FFT_HT1, KC_FFT_HT2, KC_UPDATE_G, KC_VM_VEC, KC_VM_GRAD,
+    KC_FFT2_H0, KC_FFT2_H1, KC_FFT2_H2, KC_FFT2_HT0, KC_FFT2_HT1, KC_FFT2_HT2, KC_COUNT
 };
 const char *k_names[KC_COUNT] = {"H_direct_residual", "HT_direct_update", "consensus", "H_direct_objective",
                                  "tv_value", "maxdiff", "halo_exchange", "HT_direct_plain", "H_direct_plain",
                                  "H_fft_rows", "H_fft_cols", "H_fft_rows_inv", "HT_fft_rows", "HT_fft_cols",
-                                 "HT_fft_rows_inv", "update_from_g", "vmlmb_vector", "vmlmb_grad"};
+                                 "HT_fft_rows_inv", "update_from_g", "vmlmb_vector", "vmlmb_grad",
+                                 "H_fft2_rows", "H_fft2_cols", "H_fft2_rows_inv", "HT_fft2_rows", "HT_fft2_cols",
+                                 "HT_fft2_rows_inv"};
 
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
@@ -82,6 +85,7 @@ struct deblur_ctx {
     int par = 0;
     int conv_path = DEBLUR_CONV_DIRECT;
     FftPlan *fft = nullptr;
+    FftPlan *fft2 = nullptr;              // S/2 plan for the ragged bottom / right strips of each facet
     // host copies needed after create
     std::vector<float> h_wy, h_wx;
     // communication
@@ -419,21 +423,39 @@ static deblur_status finish(deblur_t h) {
 }
 
 static deblur_status run_fft_H(deblur_t h, const FacetDev *facets, int par, int mode) {
-    for (int pass = 0; pass < 3; ++pass) {
-        cudaEvent_t ev = nullptr;
-        h->prof_begin(KC_FFT_H0 + pass, &ev);
-        CU(fft_H_pass(*h->fft, pass, facets, par, mode, h->stream));
-        h->prof_end(KC_FFT_H0 + pass, ev);
+    for (FftPlan *fp : {h->fft, h->fft2}) {
+        if (!fp) continue;
+        const int c0 = fp == h->fft ? KC_FFT_H0 : KC_FFT2_H0;
+        for (int pass = 0; pass < 3; ++pass) {
+            cudaEvent_t ev = nullptr;
+            h->prof_begin(c0 + pass, &ev);
+            CU(fft_H_pass(*fp, pass, facets, par, mode, h->stream));
+            h->prof_end(c0 + pass, ev);
+        }
     }
     return DEBLUR_OK;
 }
 
+// per-local-facet data partial sums of the last run_fft_H (both plans)
+static cudaError_t fft_partials_all(deblur_t h, std::vector<double> &out) {
+    cudaError_t e = fft_data_partials(*h->fft, out);
+    if (e != cudaSuccess || !h->fft2) return e;
+    std::vector<double> o2;
+    if ((e = fft_data_partials(*h->fft2, o2)) != cudaSuccess) return e;
+    for (size_t i = 0; i < out.size(); ++i) out[i] += o2[i];
+    return cudaSuccess;
+}
+
 static deblur_status run_fft_HT(deblur_t h, const FacetDev *facets) {
-    for (int pass = 0; pass < 3; ++pass) {
-        cudaEvent_t ev = nullptr;
-        h->prof_begin(KC_FFT_HT0 + pass, &ev);
-        CU(fft_HT_pass(*h->fft, pass, facets, h->stream));
-        h->prof_end(KC_FFT_HT0 + pass, ev);
+    for (FftPlan *fp : {h->fft, h->fft2}) {
+        if (!fp) continue;
+        const int c0 = fp == h->fft ? KC_FFT_HT0 : KC_FFT2_HT0;
+        for (int pass = 0; pass < 3; ++pass) {
+            cudaEvent_t ev = nullptr;
+            h->prof_begin(c0 + pass, &ev);
+            CU(fft_HT_pass(*fp, pass, facets, h->stream));
+            h->prof_end(c0 + pass, ev);
+        }
     }
     return DEBLUR_OK;
 }
@@ -524,6 +546,7 @@ deblur_status deblur_destroy(deblur_t h) {
     for (auto &g : h->gexec)
         if (g) { cudaGraphExecDestroy(g); g = nullptr; }
     if (h->fft) { fft_destroy(h->fft); h->fft = nullptr; }
+    if (h->fft2) { fft_destroy(h->fft2); h->fft2 = nullptr; }
     if (h->comm) { ncclCommDestroy(h->comm); h->comm = nullptr; }
     for (auto &p : h->pending) { h->ev_pool.push_back(p.a); h->ev_pool.push_back(p.b); }
     for (auto e : h->ev_pool) cudaEventDestroy(e);
@@ -803,9 +826,37 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
     // FFT path plan
     if (h->conv_path == DEBLUR_CONV_FFT) {
         std::string ferr;
+        // ragged strips: where the last row / column of S-tiles would hold at most T2 valid
+        // outputs, a plan of size S2 = S/2 covers that strip (about half the work per
+        // output column); the S plan covers the rest
+        const int S1 = fft_choose_size(P), S2 = S1 / 2, T1 = S1 - P + 1, T2 = S2 - P + 1;
+        FftRegions r1, r2;
+        bool strips = false;
+        const bool want = T2 >= 64 && !std::getenv("DEBLUR_FFT_NO_STRIPS") && !std::getenv("DEBLUR_FFT_SIZE");
+        auto bulk = [&](int m) {
+            const int t = (m + T1 - 1) / T1, rem = m - (t - 1) * T1;
+            return (want && t > 1 && rem <= T2) ? (t - 1) * T1 : m;
+        };
+        auto split = [&](int my, int mx, std::vector<FftRect> &a, std::vector<FftRect> &b) {
+            const int yb = bulk(my), xb = bulk(mx);
+            a.push_back({0, yb, 0, xb});
+            if (yb < my) b.push_back({yb, my, 0, mx});
+            if (xb < mx) b.push_back({0, yb, xb, mx});
+            strips |= (yb < my || xb < mx);
+        };
+        for (const FacetDev &F : h->fh) {
+            r1.H.emplace_back(); r1.HT.emplace_back(); r2.H.emplace_back(); r2.HT.emplace_back();
+            split(F.my, F.mx, r1.H.back(), r2.H.back());
+            split(F.ny, F.nx, r1.HT.back(), r2.HT.back());
+        }
         h->fft = fft_create(pl, h->local, h->fh, h->d_psfs, h->d_owy, h->d_owx, p->psf_gy, p->psf_gx, h->h_wy.data(),
-                            h->h_wx.data(), h->per_node, h->stream, ferr);
+                            h->h_wx.data(), h->per_node, h->stream, ferr, 0, strips ? &r1 : nullptr);
         if (!h->fft) { g_last_error = "FFT path: " + ferr; return DEBLUR_ECUDA; }
+        if (strips) {
+            h->fft2 = fft_create(pl, h->local, h->fh, h->d_psfs, h->d_owy, h->d_owx, p->psf_gy, p->psf_gx,
+                                 h->h_wy.data(), h->h_wx.data(), h->per_node, h->stream, ferr, S2, &r2);
+            if (!h->fft2) { g_last_error = "FFT path (strips): " + ferr; return DEBLUR_ECUDA; }
+        }
     }
 
     // NCCL
@@ -870,7 +921,7 @@ static deblur_status vm_eval(deblur_t h, int par_w, std::vector<float *> &Gd, st
     if (h->conv_path == DEBLUR_CONV_FFT) {
         if ((s = run_fft_H(h, h->d_facets, par_w, FFT_RESIDUAL)) != DEBLUR_OK) return s;
         CU(cudaStreamSynchronize(h->stream));
-        CU(fft_data_partials(*h->fft, data));
+        CU(fft_partials_all(h, data));
         if ((s = run_fft_HT(h, h->d_facets)) != DEBLUR_OK) return s;
     } else {
         cudaEvent_t ev = nullptr;
@@ -1149,7 +1200,7 @@ deblur_status deblur_objective(deblur_t h, double out[4]) {
         if ((s = run_fft_H(h, h->d_facets, h->par, FFT_OBJECTIVE)) != DEBLUR_OK) return s;
         CU(cudaStreamSynchronize(h->stream));
         std::vector<double> fd;
-        CU(fft_data_partials(*h->fft, fd));
+        CU(fft_partials_all(h, fd));
         for (size_t li = 0; li < h->local.size(); ++li) data[h->local[li]] = fd[li];
     } else {
         h->prof_begin(KC_H_OBJ, &ev);
@@ -1553,6 +1604,8 @@ deblur_status deblur_kernel_work(deblur_t h, int32_t cls, double *flops, double 
     }
     if (cls >= KC_FFT_H0 && cls <= KC_FFT_HT2 && h->fft)
         *bytes = fft_pass_bytes(*h->fft, cls >= KC_FFT_HT0, (cls - KC_FFT_H0) % 3);
+    if (cls >= KC_FFT2_H0 && cls <= KC_FFT2_HT2 && h->fft2)
+        *bytes = fft_pass_bytes(*h->fft2, cls >= KC_FFT2_HT0, (cls - KC_FFT2_H0) % 3);
     if (cls == KC_UPDATE_G) *bytes = 20.0 * est_px;            // g, u, x in; x+, u|v out
     if (cls == KC_HT_UPDATE) *bytes = 24.0 * est_px;           // r (~obs), x, u in; x+, u|v out
     if (cls == KC_H) *bytes = 4.0 * est_px + 12.0 * obs_px;    // x, y, W in; r out

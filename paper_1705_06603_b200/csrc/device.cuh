@@ -70,6 +70,8 @@ struct TileDesc {         // one CTA's tile
     int f;                // local facet index
     int y0, x0;           // tile origin (facet-local; observed coords for H, estimate coords for H^T)
     int p0, p1, q0, q1;   // active PSF grid rows/cols (inclusive); p1 < p0 -> none
+    int ylim = 1 << 30;   // FFT tiles: outputs only in rows < ylim, cols < xlim (the tile's region)
+    int xlim = 1 << 30;
 };
 
 struct BandRect {         // consensus work item: facet-local rectangle of band pixels

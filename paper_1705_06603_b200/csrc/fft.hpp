@@ -16,11 +16,24 @@ struct FftPlan;
 
 // Measured crossover: true when the FFT path beats the direct stencil for P.
 bool fft_prefer(int P);
+// A facet-local rectangle [y0, y1) x [x0, x1) of outputs a plan covers (observed
+// coordinates for H, estimate coordinates for H^T); tiles start at (y0, x0) and step
+// by T.  Empty lists mean the whole facet.
+struct FftRect {
+    int y0, y1, x0, x1;
+};
+struct FftRegions {
+    std::vector<std::vector<FftRect>> H, HT;   // per local facet
+};
+// FFT size for P (the plan's S) and its valid extent T = S - P + 1.
+int fft_choose_size(int P);
+
 // d_wy/d_wx: the weights applied inside H_f (all ones in per-node mode, where every
 // tile of facet (a, b) uses PSF (a, b) only); h_wy/h_wx: the interpolation weights.
 FftPlan *fft_create(const Plan &pl, const std::vector<int> &local, const std::vector<FacetDev> &fh,
                     const float *d_psfs, const float *d_wy, const float *d_wx, int Gy, int Gx, const float *h_wy,
-                    const float *h_wx, bool per_node, cudaStream_t s, std::string &err);
+                    const float *h_wx, bool per_node, cudaStream_t s, std::string &err, int S_force = 0,
+                    const FftRegions *regions = nullptr);
 void fft_destroy(FftPlan *f);
 // H on every local facet: mode RESIDUAL writes r = w (Hx - y) and data partials,
 // PLAIN writes r = Hx, OBJECTIVE only the partials.

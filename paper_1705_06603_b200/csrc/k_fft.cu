@@ -1121,7 +1121,7 @@ __global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
         for (int idx = tid; idx < nrows * T; idx += G::NTH) {
             const int rr = idx / T, cc = idx - rr * T;
             const int fy = t.y0 + r0 + rr, fx = t.x0 + cc;
-            if (fy < Fd.ny && fx < Fd.nx) Fd.g[(int64_t)fy * Fd.ep + fx] = outs[rr * XS + cc] * scale;
+            if (fy < min(Fd.ny, t.ylim) && fx < min(Fd.nx, t.xlim)) Fd.g[(int64_t)fy * Fd.ep + fx] = outs[rr * XS + cc] * scale;
         }
         return;
     }
@@ -1137,7 +1137,7 @@ __global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
             const int idx = b0 + tid + u * G::NTH;
             const int rr = idx / T, cc = idx - rr * T;
             const int oi = t.y0 + r0 + rr, oj = t.x0 + cc;
-            ok[u] = idx < ntot && oi < Fd.my && oj < Fd.mx;
+            ok[u] = idx < ntot && oi < min(Fd.my, t.ylim) && oj < min(Fd.mx, t.xlim);
             off[u] = (int64_t)oi * Fd.op + oj;
             yv[u] = (ok[u] && mode != FFT_PLAIN) ? __ldg(Fd.y + off[u]) : 0.f;
             wv[u] = (ok[u] && mode != FFT_PLAIN) ? (Fd.w ? __ldg(Fd.w + off[u]) : Fd.w_scalar) : 0.f;
@@ -1214,6 +1214,8 @@ static int choose_S(int P) {
     if (512 - P + 1 < 64 && 1024 - P + 1 >= 8) best = 1024;
     return best;
 }
+
+int fft_choose_size(int P) { return choose_S(P); }
 
 bool fft_prefer(int P) {
     // Measured crossover (profiles/r1/crossover.jsonl; 4096^2, 8x8 PSFs, 1 facet, B200):
@@ -1340,7 +1342,8 @@ static cudaError_t do_attrs(int S, int T, int NP, int NQ) {
 
 FftPlan *fft_create(const Plan &pl, const std::vector<int> &local, const std::vector<FacetDev> &fh,
                     const float *d_psfs, const float *d_wy, const float *d_wx, int Gy, int Gx, const float *h_wy,
-                    const float *h_wx, bool per_node, cudaStream_t s, std::string &err) {
+                    const float *h_wx, bool per_node, cudaStream_t s, std::string &err, int S_force,
+                    const FftRegions *regions) {
     FftPlan *f = new FftPlan();
     auto fail = [&](const std::string &m) { err = m; delete f; return (FftPlan *)nullptr; };
 #define FC(call)                                                                          \
@@ -1349,7 +1352,7 @@ FftPlan *fft_create(const Plan &pl, const std::vector<int> &local, const std::ve
         if (e_ != cudaSuccess) return fail(std::string(cudaGetErrorString(e_)) + " at " #call); \
     } while (0)
     f->P = pl.P;
-    f->S = choose_S(pl.P);
+    f->S = S_force ? S_force : choose_S(pl.P);
     if (const char *ov = std::getenv("DEBLUR_FFT_SIZE")) {      // measurement override (crossover sweeps)
         const int v = std::atoi(ov);
         if (v >= 64 && v <= 1024 && (v & (v - 1)) == 0 && v - pl.P + 1 >= 8) f->S = v;
@@ -1382,23 +1385,28 @@ FftPlan *fft_create(const Plan &pl, const std::vector<int> &local, const std::ve
             }
             range_nz(w, G, n, a, b, lo, hi);
         };
-        for (int y0 = 0; y0 < F.my; y0 += T)
-            for (int x0 = 0; x0 < F.mx; x0 += T) {
-                TileDesc t{(int)li, y0, x0, 0, -1, 0, -1};
-                range(h_wy, Gy, pl.ny, F.ey0 + y0, F.ey0 + std::min(y0 + S, F.ny), t.p0, t.p1);
-                range(h_wx, Gx, pl.nx, F.ex0 + x0, F.ex0 + std::min(x0 + S, F.nx), t.q0, t.q1);
-                if (t.q1 < t.q0) { t.q0 = 0; t.q1 = -1; }
-                f->tH.push_back(t);
-                f->tile_facet_H.push_back((int)li);
-            }
-        for (int y0 = 0; y0 < F.ny; y0 += T)
-            for (int x0 = 0; x0 < F.nx; x0 += T) {
-                TileDesc t{(int)li, y0, x0, 0, -1, 0, -1};
-                range(h_wy, Gy, pl.ny, F.ey0 + y0, F.ey0 + std::min(y0 + T, F.ny), t.p0, t.p1);
-                range(h_wx, Gx, pl.nx, F.ex0 + x0, F.ex0 + std::min(x0 + T, F.nx), t.q0, t.q1);
-                if (t.q1 < t.q0) { t.q0 = 0; t.q1 = -1; }
-                f->tHT.push_back(t);
-            }
+        const std::vector<FftRect> allH{{0, F.my, 0, F.mx}}, allHT{{0, F.ny, 0, F.nx}};
+        const auto &rH = regions ? regions->H[li] : allH;
+        const auto &rHT = regions ? regions->HT[li] : allHT;
+        for (const FftRect &R : rH)
+            for (int y0 = R.y0; y0 < R.y1; y0 += T)
+                for (int x0 = R.x0; x0 < R.x1; x0 += T) {
+                    TileDesc t{(int)li, y0, x0, 0, -1, 0, -1, R.y1, R.x1};
+                    range(h_wy, Gy, pl.ny, F.ey0 + y0, F.ey0 + std::min(y0 + S, F.ny), t.p0, t.p1);
+                    range(h_wx, Gx, pl.nx, F.ex0 + x0, F.ex0 + std::min(x0 + S, F.nx), t.q0, t.q1);
+                    if (t.q1 < t.q0) { t.q0 = 0; t.q1 = -1; }
+                    f->tH.push_back(t);
+                    f->tile_facet_H.push_back((int)li);
+                }
+        for (const FftRect &R : rHT)
+            for (int y0 = R.y0; y0 < R.y1; y0 += T)
+                for (int x0 = R.x0; x0 < R.x1; x0 += T) {
+                    TileDesc t{(int)li, y0, x0, 0, -1, 0, -1, R.y1, R.x1};
+                    range(h_wy, Gy, pl.ny, F.ey0 + y0, F.ey0 + std::min(y0 + T, F.ny), t.p0, t.p1);
+                    range(h_wx, Gx, pl.nx, F.ex0 + x0, F.ex0 + std::min(x0 + T, F.nx), t.q0, t.q1);
+                    if (t.q1 < t.q0) { t.q0 = 0; t.q1 = -1; }
+                    f->tHT.push_back(t);
+                }
     }
     for (auto *lst : {&f->tH, &f->tHT})
         for (auto &t : *lst) {

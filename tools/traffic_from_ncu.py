@@ -1,6 +1,6 @@
 """Per-launch DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) of one
 steady-state c4 iteration from an `ncu --set full` report made by
-tools/ncu_full.sh (7 launches in iteration order), written as the JSON that
+tools/ncu_full.sh (13 launches in iteration order: S plan, S/2 strip plan, update), written as the JSON that
 bench.py reads for the roofline's `traffic` field.
 
   python tools/traffic_from_ncu.py gpurun_out/p.ncu-rep profiles/r1/traffic.json
@@ -11,7 +11,8 @@ import json
 import subprocess
 import sys
 
-ORDER = ["H_fft_rows", "H_fft_cols", "H_fft_rows_inv", "HT_fft_rows", "HT_fft_cols", "HT_fft_rows_inv",
+ORDER = ["H_fft_rows", "H_fft_cols", "H_fft_rows_inv", "H_fft2_rows", "H_fft2_cols", "H_fft2_rows_inv",
+         "HT_fft_rows", "HT_fft_cols", "HT_fft_rows_inv", "HT_fft2_rows", "HT_fft2_cols", "HT_fft2_rows_inv",
          "update_from_g"]
 
 
