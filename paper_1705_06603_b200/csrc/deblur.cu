@@ -424,7 +424,7 @@ static deblur_status finish(deblur_t h) {
 
 static deblur_status run_fft_H(deblur_t h, const FacetDev *facets, int par, int mode) {
     for (FftPlan *fp : {h->fft, h->fft2}) {
-        if (!fp) continue;
+        if (!fp || !fft_tiles(*fp, false)) continue;
         const int c0 = fp == h->fft ? KC_FFT_H0 : KC_FFT2_H0;
         for (int pass = 0; pass < 3; ++pass) {
             cudaEvent_t ev = nullptr;
@@ -448,7 +448,7 @@ static cudaError_t fft_partials_all(deblur_t h, std::vector<double> &out) {
 
 static deblur_status run_fft_HT(deblur_t h, const FacetDev *facets) {
     for (FftPlan *fp : {h->fft, h->fft2}) {
-        if (!fp) continue;
+        if (!fp || !fft_tiles(*fp, true)) continue;
         const int c0 = fp == h->fft ? KC_FFT_HT0 : KC_FFT2_HT0;
         for (int pass = 0; pass < 3; ++pass) {
             cudaEvent_t ev = nullptr;

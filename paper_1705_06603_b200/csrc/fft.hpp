@@ -48,6 +48,7 @@ cudaError_t fft_HT_pass(FftPlan &f, int pass, const FacetDev *d_facets, cudaStre
 // spectra (sized to stay L2-resident) are not counted.
 double fft_pass_bytes(const FftPlan &f, bool ht, int pass);
 int fft_size(const FftPlan &f);
+int fft_tiles(const FftPlan &f, bool ht);      // tiles of the H (ht = false) or H^T tile list
 
 // per-local-facet data partial sums of the last fft_H call (after a stream sync).
 cudaError_t fft_data_partials(FftPlan &f, std::vector<double> &out);

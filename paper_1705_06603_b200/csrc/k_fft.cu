@@ -1526,6 +1526,7 @@ double fft_pass_bytes(const FftPlan &f, bool ht, int pass) {
 }
 
 int fft_size(const FftPlan &f) { return f.S; }
+int fft_tiles(const FftPlan &f, bool ht) { return (int)(ht ? f.tHT.size() : f.tH.size()); }
 
 cudaError_t fft_data_partials(FftPlan &f, std::vector<double> &out) {
     out.assign(f.nlocal, 0.0);

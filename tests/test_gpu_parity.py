@@ -363,3 +363,60 @@ def test_iterate_vmlmb(k, n, facets, O, budget, inc, iters, path):
     ro = orc.objective()
     for i in range(3):
         assert abs(obj[i] - ro[i]) <= 10 * OBJ_TOL * abs(ro[i]), (i, obj[i], ro[i])
+
+
+@pytest.mark.parametrize("rem", [193, 194, 195, 60])
+def test_fft_strip_plan_boundaries(rem):
+    """S/2 strip plan: facets whose last tile row / column holds
+    `rem` valid outputs (T = 450, T/2-plan T2 = 194 at P = 63): the strip plan is
+    used iff rem <= T2; H / H^T stay exact (vs the oracle) either way."""
+    P, T = 63, 450
+    m = T + rem                                       # one facet: observed extent T + rem per axis
+    n = m + P - 1
+    pb = synth.make_config(3, n=n, facets=(1, 1), overlap=0)
+    x, r = rand_x(pb), rand_r(pb)
+    op = oracle_op(pb)
+    with D.Deblur.from_problem(pb, conv_path=D.CONV_FFT) as dev:
+        hx = dev.apply_H(x)
+        g = dev.apply_HT(r)
+        st = dev.kernel_stats()
+    assert (st["H_fft2_cols"][0] > 0) == (rem <= 194)
+    assert (st["HT_fft2_cols"][0] > 0) == (rem + P - 1 <= 194)
+    assert rel_l2(hx, op.H(x)) <= H_TOL
+    assert rel_l2(g, op.HT(r)) <= H_TOL
+
+
+def test_fft_strips_match_single_plan(monkeypatch):
+    """The two-plan split changes only the tiling: iterates equal the single-plan
+    run within rounding."""
+    pb = synth.make_config(3, n=1024, facets=(2, 2), overlap=128)
+    with D.Deblur.from_problem(pb, conv_path=D.CONV_FFT) as dev:
+        dev.iterate(3)
+        xa, _ = dev.get_state()
+    monkeypatch.setenv("DEBLUR_FFT_NO_STRIPS", "1")
+    with D.Deblur.from_problem(pb, conv_path=D.CONV_FFT) as dev:
+        dev.iterate(3)
+        xb, _ = dev.get_state()
+    assert rel_l2(xa, xb) <= 1e-6
+
+
+@pytest.mark.parametrize("path", PATHS, ids=["direct", "fft"])
+@pytest.mark.parametrize("combo", ["node_vmlmb", "indep_vmlmb"])
+def test_combined_modes(combo, path):
+    """Per-node operators and the independent baseline with the VMLM-B Local-Solver."""
+    pb = synth.make_config(2, n=200, facets=(2, 2), overlap=20)
+    if combo == "node_vmlmb":
+        pb = synth.per_node(pb)
+    else:
+        pb.independent = 1
+    pb.local_solver, pb.inner_steps, pb.inner_increment = 1, 10, 5
+    orc = from_problem(pb)
+    with D.Deblur.from_problem(pb, conv_path=path, tau=orc.tau) as dev:
+        dev.iterate(2)
+        xs, us = dev.get_state()
+        img = dev.get_image()
+    orc.iterate(2)
+    xr, ur = orc.state()
+    assert rel_l2(xs, xr) <= IT_TOL
+    assert rel_l2(us, ur) <= IT_TOL
+    assert rel_l2(img, orc.image()) <= IT_TOL
