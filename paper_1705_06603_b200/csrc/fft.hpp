@@ -35,22 +35,18 @@ FftPlan *fft_create(const Plan &pl, const std::vector<int> &local, const std::ve
                     const float *h_wx, bool per_node, cudaStream_t s, std::string &err, int S_force = 0,
                     const FftRegions *regions = nullptr);
 void fft_destroy(FftPlan *f);
-// H on every local facet: mode RESIDUAL writes r = w (Hx - y) and data partials,
-// PLAIN writes r = Hx, OBJECTIVE only the partials.
-cudaError_t fft_H(FftPlan &f, const FacetDev *d_facets, int par, int mode, cudaStream_t s);
-// g = H^T r on every local facet (into FacetDev::g).
-cudaError_t fft_HT(FftPlan &f, const FacetDev *d_facets, cudaStream_t s);
-// single passes (0 rows forward, 1 columns, 2 rows inverse) for per-pass timing
+// H / H^T on every local facet, one pass at a time (0 rows forward, 1 columns, 2 rows
+// inverse): H mode RESIDUAL writes r = w (Hx - y) and data partials, PLAIN r = Hx,
+// OBJECTIVE only the partials; H^T writes g = H^T r into FacetDev::g
 cudaError_t fft_H_pass(FftPlan &f, int pass, const FacetDev *d_facets, int par, int mode, cudaStream_t s);
 cudaError_t fft_HT_pass(FftPlan &f, int pass, const FacetDev *d_facets, cudaStream_t s);
 // algorithmic HBM bytes moved by one launch of a pass: the pass's
 // compulsory reads/writes of x / r / y / W and of the inter-pass spectra; the PSF
 // spectra (sized to stay L2-resident) are not counted.
 double fft_pass_bytes(const FftPlan &f, bool ht, int pass);
-int fft_size(const FftPlan &f);
 int fft_tiles(const FftPlan &f, bool ht);      // tiles of the H (ht = false) or H^T tile list
 
-// per-local-facet data partial sums of the last fft_H call (after a stream sync).
+// per-local-facet data partial sums of the last H pass 2 (after a stream sync).
 cudaError_t fft_data_partials(FftPlan &f, std::vector<double> &out);
 
 }  // namespace deblur

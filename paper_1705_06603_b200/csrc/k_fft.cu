@@ -1471,24 +1471,6 @@ FftPlan *fft_create(const Plan &pl, const std::vector<int> &local, const std::ve
 
 void fft_destroy(FftPlan *f) { delete f; }
 
-cudaError_t fft_H(FftPlan &f, const FacetDev *d_facets, int par, int mode, cudaStream_t s) {
-    FftArgs a = f.args(d_facets, false);
-    const int n = (int)f.tH.size();
-    cudaError_t e;
-    if ((e = do_rows_fwd(f.S, a, n, 0, par, nullptr, 0, nullptr, s)) != cudaSuccess) return e;
-    if ((e = do_cols(f.S, a, n, 0, nullptr, nullptr, 0, s)) != cudaSuccess) return e;
-    return do_rows_inv(f.S, a, n, f.T, mode, s);
-}
-
-cudaError_t fft_HT(FftPlan &f, const FacetDev *d_facets, cudaStream_t s) {
-    FftArgs a = f.args(d_facets, true);
-    const int n = (int)f.tHT.size();
-    cudaError_t e;
-    if ((e = do_rows_fwd(f.S, a, n, 1, 0, nullptr, 0, nullptr, s)) != cudaSuccess) return e;
-    if ((e = do_cols(f.S, a, n, 1, nullptr, nullptr, 0, s)) != cudaSuccess) return e;
-    return do_rows_inv(f.S, a, n, f.T, INV_HT, s);
-}
-
 cudaError_t fft_H_pass(FftPlan &f, int pass, const FacetDev *d_facets, int par, int mode, cudaStream_t s) {
     FftArgs a = f.args(d_facets, false);
     const int n = (int)f.tH.size();
@@ -1525,7 +1507,6 @@ double fft_pass_bytes(const FftPlan &f, bool ht, int pass) {
     return b;
 }
 
-int fft_size(const FftPlan &f) { return f.S; }
 int fft_tiles(const FftPlan &f, bool ht) { return (int)(ht ? f.tHT.size() : f.tH.size()); }
 
 cudaError_t fft_data_partials(FftPlan &f, std::vector<double> &out) {
