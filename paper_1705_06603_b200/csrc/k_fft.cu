@@ -35,6 +35,10 @@
 #ifndef COLS_TMEM
 #define COLS_TMEM 1
 #endif
+#ifndef COLS_TM_TWHALF
+#define COLS_TM_TWHALF 1
+#endif
+#define COLS_TM_TW (COLS_TM_TWHALF ? S / 2 : S)
 #ifndef COLS_TM_NB
 #define COLS_TM_NB 8
 #endif
@@ -753,7 +757,7 @@ struct GCT {
 template <int S>
 static size_t smem_cols_tm(int NP, int NQ) {
     using G = GCT<S>;
-    return (size_t)S * 8 + (size_t)S * G::NB * 8 + (size_t)G::NB * G::CS * 8 + (size_t)NP * S * 4 +
+    return (size_t)COLS_TM_TW * 8 + (size_t)S * G::NB * 8 + (size_t)G::NB * G::CS * 8 + (size_t)NP * S * 4 +
            (size_t)NP * NQ * 4 + 16;
 }
 
@@ -768,7 +772,7 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
     static_assert(LD<S>::LDF == S / 2 + NB, "chunking shared with k_cols");
     extern __shared__ __align__(16) float2 sm2[];
     float2 *Wsm = sm2;               // S
-    float2 *hbuf = Wsm + S;          // S x NB (prefetched PSF spectrum chunk, pair-interleaved)
+    float2 *hbuf = Wsm + COLS_TM_TW; // S x NB (prefetched PSF spectrum chunk, pair-interleaved)
     float2 *work = hbuf + S * NB;    // NB x CS
     float *wys_all = reinterpret_cast<float *>(work + NB * CS);
     int *slot_s = reinterpret_cast<int *>(wys_all + (size_t)A.NP * S);
@@ -782,7 +786,7 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
                      :: "r"((uint32_t)__cvta_generic_to_shared(tm_slot)), "n"(G::TMCOLS) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
     }
-    for (int i = tid; i < S; i += NTH) Wsm[i] = A.W[i];
+    for (int i = tid; i < COLS_TM_TW; i += NTH) Wsm[i] = A.W[i];   // a length-S forward/inverse plan uses W^k, k < S/2
     const TileDesc td = A.tiles[tile];
     const FacetDev &Fd = A.facets[td.f];
     float2 *base = A.scratch + (int64_t)tile * A.tile_rows * LDF;
