@@ -35,6 +35,12 @@
 #ifndef COLS_TMEM
 #define COLS_TMEM 1
 #endif
+// row passes: a length-S/2 plan over an S table uses W^k, k < S/2, and the R2C / C2R
+// pre/post twiddles W^k, k <= S/2: S/2 + 2 entries (16-byte multiple)
+#ifndef ROWS_TWHALF
+#define ROWS_TWHALF 1
+#endif
+#define ROWS_TW(S) (ROWS_TWHALF ? (S) / 2 + 2 : (S))
 #ifndef COLS_TM_TWHALF
 #define COLS_TM_TWHALF 1
 #endif
@@ -318,8 +324,8 @@ __global__ void __launch_bounds__(256) k_rows_fwd(FftArgs A, int mode, int par, 
     using F = typename G::F;
     constexpr int NB = G::NB, SH = G::SH, NF = G::NF, RS = G::RS, XS = G::XS, LDF = LD<S>::LDF;
     extern __shared__ __align__(16) float2 sm2[];
-    float2 *Wsm = sm2;                                      // S
-    float2 *work = Wsm + S;                                 // NB x RS
+    float2 *Wsm = sm2;                                      // ROWS_TW(S) twiddles
+    float2 *work = Wsm + ROWS_TW(S);                        // NB x RS
     float *xs = reinterpret_cast<float *>(work + NB * RS);  // NB x XS
     float *wxs = xs + NB * XS;                              // S
     const int tid = threadIdx.x;
@@ -336,7 +342,7 @@ __global__ void __launch_bounds__(256) k_rows_fwd(FftArgs A, int mode, int par, 
         Fd = &A.facets[t.f];
         if (mode == 0) { q0 = t.q0; nq = t.q1 - t.q0 + 1; }
     }
-    for (int i = tid; i < S; i += G::NTH) Wsm[i] = A.W[i];
+    for (int i = tid; i < ROWS_TW(S); i += G::NTH) Wsm[i] = A.W[i];
     {
         // batched loads (all in flight before the first use): real rows of the window
         constexpr int LPT = NB * S / G::NTH;
@@ -1046,8 +1052,8 @@ __global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
     constexpr int NB = G::NB, RS = G::RS, XS = G::XS, LDF = LD<S>::LDF, E = G::E;
     static_assert(XS <= 2 * RS, "outs aliases work");
     extern __shared__ __align__(16) float2 sm2[];
-    float2 *Wsm = sm2;
-    float2 *work = Wsm + S;                                    // NB x RS; reused as outs (NB x XS reals)
+    float2 *Wsm = sm2;                                         // ROWS_TW(S) twiddles
+    float2 *work = Wsm + ROWS_TW(S);                           // NB x RS; reused as outs (NB x XS reals)
     float2 *stg = work + NB * RS;                              // NB x SS staging
     float *wxs = reinterpret_cast<float *>(stg + NB * C::SS);  // NQ x S (H^T)
     float *outs = reinterpret_cast<float *>(work);
@@ -1068,7 +1074,7 @@ __global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
         return ht ? Bbase + ((int64_t)qi * T + r0) * LDF : base + ((int64_t)A.NQ * S + r0) * LDF;
     };
     if (nq > 0) C::issue(stg, src(0), nrows, tid);
-    for (int i = tid; i < S; i += G::NTH) Wsm[i] = A.W[i];
+    for (int i = tid; i < ROWS_TW(S); i += G::NTH) Wsm[i] = A.W[i];
     if (ht) {
         for (int idx = tid; idx < nq * S; idx += G::NTH) {
             const int qi = idx / S, cc = idx - qi * S;
@@ -1230,7 +1236,7 @@ bool fft_prefer(int P) {
 template <int S>
 static size_t smem_rows_fwd() {
     using G = GR<S>;
-    return (size_t)S * 8 + (size_t)G::NB * G::RS * 8 + (size_t)G::NB * G::XS * 4 + (size_t)S * 4;
+    return (size_t)ROWS_TW(S) * 8 + (size_t)G::NB * G::RS * 8 + (size_t)G::NB * G::XS * 4 + (size_t)S * 4;
 }
 template <int S>
 static size_t smem_cols(int NP, int NQ) {
@@ -1240,7 +1246,8 @@ static size_t smem_cols(int NP, int NQ) {
 template <int S>
 static size_t smem_rows_inv(int NQ, bool ht = true) {
     using G = GR<S>;
-    return (size_t)S * 8 + (size_t)G::NB * G::RS * 8 + (size_t)G::NB * C2R<S>::SS * 8 + (ht ? (size_t)NQ * S * 4 : 0);
+    return (size_t)ROWS_TW(S) * 8 + (size_t)G::NB * G::RS * 8 + (size_t)G::NB * C2R<S>::SS * 8 +
+           (ht ? (size_t)NQ * S * 4 : 0);
 }
 
 // The dynamic-shared-memory limit is a property of the kernel function, shared by
