@@ -93,6 +93,13 @@ CONFIGS = {
             noise=("gauss", 0.005), facets=(4, 2), overlap=128, iters=50),
     5: dict(n=32768, P=127, G=32, psf="moffat_elliptic", sources=2000000, galaxies=0,
             noise=("gauss", 0.005), facets=(8, 8), overlap=192, iters=20),
+    # c6: the paper's shift-variant experiment shape (SURVEY §8d
+    # "optional paper-shaped config", NEXT-4): 1151 x 1407 at 6000 photons/pixel, sigma^2 =
+    # 400, 9 x 9 Gaussian PSFs of 201 x 201, Huber delta = 100, lambda = 0.002, gamma =
+    # 0.4 W = 0.001, 25 iterations; a star field stands in for the photograph.
+    6: dict(n=1151, nx=1407, P=201, G=9, psf="paper_gauss", sources=3000, galaxies=300,
+            noise=("gauss", 20.0), scale=6000.0, facets=(3, 3), overlap=64, iters=25,
+            reg_kind=1, eps=100.0, lam=0.002),
 }
 
 GAIN_E = 1000.0     # Poisson gain for the mixed-noise config
@@ -193,6 +200,15 @@ def psf_grid(kind: str, G: int, P: int, rng: np.random.Generator):
                 v = -X * math.sin(th) + Y * math.cos(th)
                 h = (1.0 + (u / al) ** 2 + (v / (al * (1.0 - e))) ** 2) ** (-beta)
                 s_eq = fwhm * math.sqrt(1.0 - e) / 2.3548
+            elif kind == "paper_gauss":  # c6: FWHM 3.5 x 3.5 at the centre, growing
+                r = rh[p, q]               # linearly with the radius to 16.5 x 10.5 at the corners (coma-like)
+                fmaj, fmin = 3.5 + 13.0 * r, 3.5 + 7.0 * r
+                smaj, smin = fmaj / 2.3548, fmin / 2.3548
+                th = ang[p, q]
+                u = X * math.cos(th) + Y * math.sin(th)
+                v = -X * math.sin(th) + Y * math.cos(th)
+                h = np.exp(-0.5 * ((u / smaj) ** 2 + (v / smin) ** 2))
+                s_eq = math.sqrt(smaj * smin)
             else:
                 raise ValueError(kind)
             out[p * G + q] = h / h.sum()
@@ -244,20 +260,23 @@ def _local_sigma(sig: np.ndarray, wy: np.ndarray, wx: np.ndarray, r: np.ndarray,
 
 
 def render_observed(n: int, P: int, sig: np.ndarray, wy: np.ndarray, wx: np.ndarray,
-                    n_src: int, n_gal: int, rng_src, rng_gal) -> np.ndarray:
-    """Noiseless observed image (M x M, fp64) of a star field (+ galaxies) seen
-    through the PSF grid, rendered analytically (see module docstring)."""
+                    n_src: int, n_gal: int, rng_src, rng_gal, nx: Optional[int] = None) -> np.ndarray:
+    """Noiseless observed image (M_y x M_x, fp64) of a star field (+ galaxies) seen
+    through the PSF grid, rendered analytically (see module docstring).  The scene
+    is n x nx (nx = n if not given)."""
+    ny = n
+    nx = n if nx is None else nx
     c = (P - 1) // 2
-    M = n - P + 1
-    img = np.zeros((M, M))
+    My, Mx = ny - P + 1, nx - P + 1
+    img = np.zeros((My, Mx))
     # smooth background 0.05 + 0.02*(c1 u + c2 v + c3 uv + c4 u^2 + c5 v^2), clipped >= 0
     cc = rng_src.uniform(-1, 1, 5)
-    u = np.linspace(-1, 1, n)[c:c + M]
-    U, V = u[None, :], u[:, None]
+    U = np.linspace(-1, 1, nx)[c:c + Mx][None, :]
+    V = np.linspace(-1, 1, ny)[c:c + My][:, None]
     img += np.maximum(0.0, 0.05 + 0.02 * (cc[0] * U + cc[1] * V + cc[2] * U * V + cc[3] * U ** 2 + cc[4] * V ** 2))
     # point sources: position U[0,n)^2 (estimate coords), peak U(0.2,1), sigma U(0.5,1.5)
-    pr = rng_src.uniform(0, n, n_src)
-    pc = rng_src.uniform(0, n, n_src)
+    pr = rng_src.uniform(0, ny, n_src)
+    pc = rng_src.uniform(0, nx, n_src)
     amp = rng_src.uniform(0.2, 1.0, n_src)
     ss = rng_src.uniform(0.5, 1.5, n_src)
     sp = _local_sigma(sig, wy, wx, pr, pc)
@@ -267,7 +286,7 @@ def render_observed(n: int, P: int, sig: np.ndarray, wy: np.ndarray, wx: np.ndar
     _splat(img, pr - c, pc - c, A, s2, R)
     # extended elliptical galaxies (c3): sigma_major U(2,12), ratio U(0.3,1), angle U(0,pi), peak U(0.02,0.3)
     for _ in range(n_gal):
-        gr, gc = rng_gal.uniform(0, n, 2)
+        gr, gc = rng_gal.uniform(0, ny), rng_gal.uniform(0, nx)
         smaj = rng_gal.uniform(2, 12)
         smin = smaj * rng_gal.uniform(0.3, 1.0)
         th = rng_gal.uniform(0, math.pi)
@@ -280,8 +299,8 @@ def render_observed(n: int, P: int, sig: np.ndarray, wy: np.ndarray, wx: np.ndar
         Si = np.linalg.inv(St)
         Rg = int(math.ceil(4.0 * math.sqrt(max(np.linalg.eigvalsh(St)))))
         r0, c0 = gr - c, gc - c
-        i0, i1 = max(0, int(r0) - Rg), min(M, int(r0) + Rg + 1)
-        j0, j1 = max(0, int(c0) - Rg), min(M, int(c0) + Rg + 1)
+        i0, i1 = max(0, int(r0) - Rg), min(My, int(r0) + Rg + 1)
+        j0, j1 = max(0, int(c0) - Rg), min(Mx, int(c0) + Rg + 1)
         if i0 >= i1 or j0 >= j1:
             continue
         dy = np.arange(i0, i1)[:, None] - r0
@@ -308,7 +327,7 @@ def make_problem(name: str, n: int, P: int, G: int, psf: str, sources: int, gala
                  noise, facets, overlap: int, iters: int, seed: int, nx: Optional[int] = None,
                  lam: float = 0.01, eps: float = 1e-3, rho: float = 1.0, inner_steps: int = 1,
                  reg_kind: int = 0, tv_boundary: int = 0, gamma: Optional[float] = None,
-                 Gx: Optional[int] = None) -> Problem:
+                 Gx: Optional[int] = None, scale: float = 1.0) -> Problem:
     ny = n
     nx = n if nx is None else nx
     Gy = G
@@ -323,9 +342,8 @@ def make_problem(name: str, n: int, P: int, G: int, psf: str, sources: int, gala
         sig = sig[:Gy, :Gx]
     wy64 = hat_weights(ny, Gy)
     wx64 = hat_weights(nx, Gx)
-    if ny != nx:
-        raise NotImplementedError("renderer is square; pass nx=None")
-    clean = render_observed(n, P, sig, wy64, wx64, sources, galaxies, rng_src, rng_gal)
+    # scale: photons per unit of the star-field intensity (the paper's 6000-photon images)
+    clean = scale * render_observed(n, P, sig, wy64, wx64, sources, galaxies, rng_src, rng_gal, nx=nx)
     kind, sigma = noise
     if kind == "gauss":
         y = clean + sigma * rng_noise.standard_normal(clean.shape)
@@ -359,6 +377,8 @@ def make_config(k: int, n: Optional[int] = None, **over) -> Problem:
         scale = (n / full_n) ** 2
         cfg["sources"] = max(1, int(round(cfg["sources"] * scale)))
         cfg["galaxies"] = int(round(cfg["galaxies"] * scale))
+        if "nx" in cfg:                  # keep the aspect ratio
+            cfg["nx"] = int(round(cfg["nx"] * n / full_n))
         cfg["n"] = n
     cfg.update(over)
     return make_problem(name=f"c{k}" + ("" if n in (None, full_n) else f"@{n}"), seed=1000 * k, **cfg)

@@ -136,3 +136,44 @@ def test_apply_c5_sampled(count):
     ei[:4] = [0, pb.ny - 1, 63, pb.ny - 64]
     ref = op.HT_points(r, ei, ej)
     assert rel_l2(g[ei, ej], ref) <= H_TOL
+
+
+def test_paper_shaped_c6_apply_sampled():
+    """c6, the paper's shift-variant experiment shape: 1151 x 1407,
+    9 x 9 Gaussian PSFs of 201 x 201 (FFT path, S = 512, T = 312); 2 x 2 facets
+    with overlap P - 1 = 200 (the owner-computes apply_HT needs O >= P - 1, §8b);
+    H / H^T on sampled pixels including facet seams and the image borders."""
+    pb = synth.make_config(6, facets=(2, 2), overlap=200)
+    rng = np.random.default_rng(66)
+    x = (6000.0 * rng.random((pb.ny, pb.nx))).astype(np.float32)
+    r = rng.standard_normal((pb.my, pb.mx)).astype(np.float32)
+    op = Operator(pb.psfs, pb.wy, pb.wx)
+    with D.Deblur.from_problem(pb) as dev:
+        assert dev.conv_path == D.CONV_FFT
+        hx = dev.apply_H(x)
+        g = dev.apply_HT(r)
+    oi, oj = rng.integers(0, pb.my, 1500), rng.integers(0, pb.mx, 1500)
+    oi[:4] = [0, pb.my - 1, pb.my // 3, 2 * pb.my // 3]
+    assert rel_l2(hx[oi, oj], op.H_points(x, oi, oj)) <= H_TOL
+    ei, ej = rng.integers(0, pb.ny, 1500), rng.integers(0, pb.nx, 1500)
+    ei[:4] = [0, pb.ny - 1, 100, pb.ny - 101]
+    assert rel_l2(g[ei, ej], op.HT_points(r, ei, ej)) <= H_TOL
+
+
+def test_paper_shaped_c6_iterate_small():
+    """c6 parameters (Huber delta = 100, lambda = 0.002, gamma = 0.001, 6000-photon
+    scale, P = 201) on a 400 x 489 crop of the geometry: 2 iterations vs the oracle."""
+    from oracle import from_problem
+    pb = synth.make_config(6, n=400, facets=(1, 1), overlap=0)
+    orc = from_problem(pb)
+    with D.Deblur.from_problem(pb, tau=orc.tau) as dev:
+        dev.iterate(2)
+        xs, us = dev.get_state()
+        obj = dev.objective()
+    orc.iterate(2)
+    xr, ur = orc.state()
+    assert rel_l2(xs, xr) <= IT_TOL
+    assert rel_l2(us, ur) <= IT_TOL
+    ro = orc.objective()
+    for i in range(3):
+        assert abs(obj[i] - ro[i]) <= 1e-4 * abs(ro[i]), (i, obj[i], ro[i])
