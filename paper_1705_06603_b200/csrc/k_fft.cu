@@ -860,23 +860,22 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
                 for (int h = 0; h < 2; ++h) {
                     uint32_t a[16];
                     if (!first) { tm_ld16(t_acc + 16 * h, a); tm_wait_ld(); }
+                    // half h = butterflies [h BPT/2, (h+1) BPT/2): 8-byte loads of their own
+                    // spectrum values (a half never holds both members of a 16-byte pair)
 #pragma unroll
-                    for (int i2 = 0; i2 < SL::BPT / 2; i2 += 2) {
+                    for (int i2 = 0; i2 < SL::BPT / 2; ++i2) {
                         const int i = h * (SL::BPT / 2) + i2;
                         int t, j;
                         SL::bj(i, tid, t, j);
 #pragma unroll
                         for (int r = 0; r < SL::R; ++r) {
-                            const float4 hh = ld4(hbuf + hb_idx<NB>(SL::out_n(j, r), t));
-                            const float2 p0 = cmul(v[i * SL::R + r], lo2(hh));
-                            const float2 p1 = cmul(v[(i + 1) * SL::R + r], hi2(hh));
-                            const int e0 = (i2 * SL::R + r) * 2, e1 = ((i2 + 1) * SL::R + r) * 2;
-                            float2 a0 = first ? make_float2(0.f, 0.f) : make_float2(__uint_as_float(a[e0]), __uint_as_float(a[e0 + 1]));
-                            float2 a1 = first ? make_float2(0.f, 0.f) : make_float2(__uint_as_float(a[e1]), __uint_as_float(a[e1 + 1]));
+                            const float2 hv = hbuf[hb_idx<NB>(SL::out_n(j, r), t)];
+                            const float2 p0 = cmul(v[i * SL::R + r], hv);
+                            const int e = (i2 * SL::R + r) * 2;
+                            float2 a0 = first ? make_float2(0.f, 0.f) : make_float2(__uint_as_float(a[e]), __uint_as_float(a[e + 1]));
                             a0 = cadd(a0, p0);
-                            a1 = cadd(a1, p1);
-                            a[e0] = __float_as_uint(a0.x); a[e0 + 1] = __float_as_uint(a0.y);
-                            a[e1] = __float_as_uint(a1.x); a[e1 + 1] = __float_as_uint(a1.y);
+                            a[e] = __float_as_uint(a0.x);
+                            a[e + 1] = __float_as_uint(a0.y);
                         }
                     }
                     tm_st16(t_acc + 16 * h, a);
