@@ -53,28 +53,40 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """nvidia-smi clocks + throttle reasons, sampled every 50 ms from before the timed
+    region (nvidia-smi needs ~0.1-0.3 s to start) and filtered to the samples taken
+    between mark_start() and mark_end() (host wall clock; the region is bracketed by
+    device synchronisation, so wall time covers the device work)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
         self.device = device
         self.p = None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.5)                     # let NVML start before the timed region
         except Exception:
             self.p = None
         return self
 
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
     def __exit__(self, *a):
         self.out = ""
         if self.p is not None:
+            time.sleep(0.1)
             self.p.terminate()
             try:
                 self.out, _ = self.p.communicate(timeout=5)
@@ -82,18 +94,24 @@ class ClockSampler:
                 self.p.kill()
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
+        import datetime
+        sm, mx, reasons, outside = [], 0.0, set(), 0
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in (self.out or "").strip().splitlines():
             f = [s.strip() for s in line.split(",")]
-            if len(f) < 9:
+            if len(f) < 10:
                 continue
             try:
-                sm.append(float(f[1]))
-                mx = max(mx, float(f[2]))
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                clk, cmax = float(f[2]), float(f[3])
             except ValueError:
                 continue
-            for nm, v in zip(names, f[5:9]):
+            if self.t0 is not None and self.t1 is not None and not (self.t0 <= ts <= self.t1):
+                outside += 1
+                continue
+            sm.append(clk)
+            mx = max(mx, cmax)
+            for nm, v in zip(names, f[6:10]):
                 if v.lower() == "active":
                     reasons.add(nm)
         if not sm:
@@ -138,10 +156,12 @@ def run_ours(args, rank, world, local):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = sum(v[0] for k, v in dev.kernel_stats().items() if k != "halo_exchange")
     with ClockSampler(local) as clk:
+        clk.mark_start()
         e0.record(stream)
         dev.iterate(args.steps)                       # the timed region: no instrumentation
         e1.record(stream)
         barrier()
+        clk.mark_end()
     ms = e0.elapsed_time(e1)
     launches = sum(v[0] for k, v in dev.kernel_stats().items() if k != "halo_exchange") - launches0
     # second pass over the same K steps with per-kernel CUDA events on the library stream
@@ -327,7 +347,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
