@@ -420,3 +420,20 @@ def test_combined_modes(combo, path):
     assert rel_l2(xs, xr) <= IT_TOL
     assert rel_l2(us, ur) <= IT_TOL
     assert rel_l2(img, orc.image()) <= IT_TOL
+
+
+def test_vmlmb_reset_restarts_the_budget_schedule():
+    """deblur_reset starts a fresh solve: the VMLM-B budget (inner_steps + k inner_increment)
+    restarts at k = 0, so reset + n iterations == a fresh handle's n iterations."""
+    pb = synth.make_config(2, n=200, facets=(2, 2), overlap=20)
+    pb.local_solver, pb.inner_steps, pb.inner_increment = 1, 5, 5
+    with D.Deblur.from_problem(pb, conv_path=D.CONV_FFT) as dev:
+        dev.iterate(2)
+        dev.reset(pb.y)
+        dev.iterate(2)
+        xa, ua = dev.get_state()
+    with D.Deblur.from_problem(pb, conv_path=D.CONV_FFT) as dev:
+        dev.iterate(2)
+        xb, ub = dev.get_state()
+    np.testing.assert_array_equal(xa, xb)
+    np.testing.assert_array_equal(ua, ub)

@@ -69,7 +69,11 @@ def test_planner_messages_are_pairwise_consistent():
 
 @pytest.mark.parametrize("field,value,needle", [("rho", 2.0, "rho"), ("eps", 0.0, "eps"), ("overlap", 3, "overlap"),
                                                 ("inner_steps", 0, "inner_steps"), ("psf_size", 4, "psf_size"),
-                                                ("world", 5, "world")])
+                                                ("world", 5, "world"), ("operator_mode", 2, "operator_mode"),
+                                                ("operator_mode", 1, "facet grid"), ("independent", 3, "independent"),
+                                                ("local_solver", 2, "local_solver"),
+                                                ("inner_increment", -1, "inner_increment"),
+                                                ("abi_version", 1, "abi_version")])
 def test_validation_names_argument(field, value, needle):
     params, keep, pb = small_params()
     setattr(params, field, value)
