@@ -82,6 +82,21 @@ __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
+// R2C post step for bin k from Z_k, Z_{SH-k} and W_S^k: (Z_k + Z*_{SH-k})/2 - i/2 W^k (Z_k - Z*_{SH-k})
+__device__ __forceinline__ float2 r2c_post(float2 zk, float2 zp, float2 w) {
+    const float2 sh = make_float2(0.5f * (zk.x + zp.x), 0.5f * (zk.y - zp.y));
+    const float2 d = make_float2(0.5f * (zk.x - zp.x), 0.5f * (zk.y + zp.y));
+    const float2 wd = cmul(w, d);
+    return make_float2(sh.x + wd.y, sh.y - wd.x);
+}
+// C2R pre step for bin k from X_k, X_{SH-k} and W_S^k: E + i O with E = (X_k + X*_{SH-k})/2,
+// O = (X_k - X*_{SH-k})/2 conj(W^k)
+__device__ __forceinline__ float2 c2r_pre(float2 xk, float2 xp, float2 w) {
+    const float2 e = make_float2(0.5f * (xk.x + xp.x), 0.5f * (xk.y - xp.y));
+    const float2 d = make_float2(0.5f * (xk.x - xp.x), 0.5f * (xk.y + xp.y));
+    const float2 o = cmul(d, conjf2(w));
+    return make_float2(e.x - o.y, e.y + o.x);
+}
 
 // v * (SIGN < 0 ? -i : +i)
 template <int SIGN>
@@ -292,7 +307,7 @@ struct Fft {
 // geometry of the row passes (length SH complex transforms, NBR rows per CTA)
 template <int S>
 struct GR {
-    static constexpr int SH = S / 2, NF = SH + 1;
+    static constexpr int SH = S / 2;
     static constexpr int NTH = 256;
     static constexpr int NB = (S <= 64) ? 64 : (S <= 128) ? 32 : 16;
     static constexpr int RS = SH + 2;    // smem row stride (float2): even (16-byte pair exchanges), conflict-free
@@ -322,7 +337,7 @@ __global__ void __launch_bounds__(256) k_rows_fwd(FftArgs A, int mode, int par, 
                                                   float2 *hrows) {
     using G = GR<S>;
     using F = typename G::F;
-    constexpr int NB = G::NB, SH = G::SH, NF = G::NF, RS = G::RS, XS = G::XS, LDF = LD<S>::LDF;
+    constexpr int NB = G::NB, SH = G::SH, RS = G::RS, XS = G::XS, LDF = LD<S>::LDF;
     extern __shared__ __align__(16) float2 sm2[];
     float2 *Wsm = sm2;                                      // ROWS_TW(S) twiddles
     float2 *work = Wsm + ROWS_TW(S);                        // NB x RS
@@ -400,21 +415,21 @@ __global__ void __launch_bounds__(256) k_rows_fwd(FftArgs A, int mode, int par, 
         F::template middle<-1>(work, v, tid, Wsm, S);
         F::Last::store(work, v, tid);
         __syncthreads();
-        // R2C post-processing: X[k] = (Zk + conj Z_{SH-k})/2 - i/2 W_S^k (Zk - conj Z_{SH-k})
-        for (int idx = tid; idx < NB * NF; idx += G::NTH) {
-            const int rr = idx / NF, k = idx - rr * NF;
-            const float2 zk = work[rr * RS + (k & (SH - 1))];
-            const float2 zc = conjf2(work[rr * RS + ((SH - k) & (SH - 1))]);
-            const float2 sh = make_float2(0.5f * (zk.x + zc.x), 0.5f * (zk.y + zc.y));
-            const float2 d = make_float2(0.5f * (zk.x - zc.x), 0.5f * (zk.y - zc.y));
-            const float2 wd = cmul(Wsm[k & (S - 1)], d);
-            const float2 X = make_float2(sh.x + wd.y, sh.y - wd.x);
-            float2 *dst;
-            if (mode == 2)
-                dst = hrows + ((int64_t)tile * S + r0 + rr) * LDF;
-            else
-                dst = A.scratch + (int64_t)tile * A.tile_rows * LDF + ((int64_t)qi * S + r0 + rr) * LDF;
-            dst[k] = X;
+        // R2C post-processing, one (k, SH - k) pair per item (both outputs read the same two
+        // values; W^{SH-k} = -conj W^k); the self-paired k = SH/2 is done by the k = 0 item
+        constexpr int HP = SH / 2;
+        for (int idx = tid; idx < NB * HP; idx += G::NTH) {
+            const int rr = idx / HP, k = idx % HP;
+            const float2 *wr = work + rr * RS;
+            float2 *dst = (mode == 2) ? hrows + ((int64_t)tile * S + r0 + rr) * LDF
+                                      : A.scratch + (int64_t)tile * A.tile_rows * LDF + ((int64_t)qi * S + r0 + rr) * LDF;
+            const float2 a = wr[k], b = wr[(SH - k) & (SH - 1)], w = Wsm[k];
+            dst[k] = r2c_post(a, b, w);
+            dst[SH - k] = r2c_post(b, a, make_float2(-w.x, w.y));
+            if (k == 0) {
+                const float2 m = wr[HP];
+                dst[HP] = r2c_post(m, m, Wsm[HP]);
+            }
         }
     }
 }
@@ -1028,16 +1043,22 @@ struct C2R {
         }
         __pipeline_commit();
     }
-    // half-length complex input z = E + i O from the staged spectrum rows -> work
+    // half-length complex input z = E + i O from the staged spectrum rows -> work, one
+    // (k, SH - k) pair per item; the self-paired k = SH/2 is done by the k = 0 item
     __device__ static __forceinline__ void pre(float2 *work, const float2 *stg, const float2 *Wsm, int tid) {
-        for (int idx = tid; idx < NB * SH; idx += G::NTH) {
-            const int rr = idx / SH, k = idx - rr * SH;
-            const float2 xk = stg[rr * SS + k];
-            const float2 b = conjf2(stg[rr * SS + SH - k]);
-            const float2 e = make_float2(0.5f * (xk.x + b.x), 0.5f * (xk.y + b.y));
-            const float2 d = make_float2(0.5f * (xk.x - b.x), 0.5f * (xk.y - b.y));
-            const float2 o = cmul(d, conjf2(Wsm[k]));     // O_k
-            work[rr * RS + k] = make_float2(e.x - o.y, e.y + o.x);   // E + i O
+        constexpr int HP = SH / 2;
+        for (int idx = tid; idx < NB * HP; idx += G::NTH) {
+            const int rr = idx / HP, k = idx % HP;
+            const float2 *sr = stg + rr * SS;
+            float2 *wr = work + rr * RS;
+            const float2 a = sr[k], b = sr[SH - k], w = Wsm[k];
+            wr[k] = c2r_pre(a, b, w);
+            if (k == 0) {
+                const float2 m = sr[HP];
+                wr[HP] = c2r_pre(m, m, Wsm[HP]);
+            } else {
+                wr[SH - k] = c2r_pre(b, a, make_float2(-w.x, w.y));
+            }
         }
     }
 };
@@ -1126,42 +1147,53 @@ __global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
     }
     __syncthreads();
 
+    // valid outputs of this row block: rows [0, nr), columns [0, nc) (facet edge and
+    // strip clip); the flat index walks (rr, cc) incrementally (no per-element division)
+    const int ny_ = ht ? Fd.ny : Fd.my, nx_ = ht ? Fd.nx : Fd.mx;
+    const int nr = min(nrows, min(ny_, t.ylim) - (t.y0 + r0)), nc = min(T, min(nx_, t.xlim) - t.x0);
+    if (nr <= 0 || nc <= 0) {
+        if (!ht && mode != FFT_PLAIN && A.partials && tid == 0) A.partials[blockIdx.x] = 0.0;
+        return;
+    }
+    const int ntot = nr * nc, drr = G::NTH / nc, dcc = G::NTH - drr * nc;
+    int rr = tid / nc, cc = tid - rr * nc;
+    auto step = [&]() {
+        rr += drr;
+        cc += dcc;
+        if (cc >= nc) { cc -= nc; ++rr; }
+    };
     if (ht) {
-        for (int idx = tid; idx < nrows * T; idx += G::NTH) {
-            const int rr = idx / T, cc = idx - rr * T;
-            const int fy = t.y0 + r0 + rr, fx = t.x0 + cc;
-            if (fy < min(Fd.ny, t.ylim) && fx < min(Fd.nx, t.xlim)) Fd.g[(int64_t)fy * Fd.ep + fx] = outs[rr * XS + cc] * scale;
-        }
+        float *gb = Fd.g + (int64_t)(t.y0 + r0) * Fd.ep + t.x0;
+        for (int idx = tid; idx < ntot; idx += G::NTH, step()) gb[rr * Fd.ep + cc] = outs[rr * XS + cc] * scale;
         return;
     }
     double dsum = 0.0;
     constexpr int U = 8;
-    const int ntot = nrows * T;
+    const int64_t obase = (int64_t)(t.y0 + r0) * Fd.op + t.x0;
+    const float *yb = Fd.y + obase, *wb = Fd.w ? Fd.w + obase : nullptr;
+    float *rb = Fd.r + obase;
     for (int b0 = 0; b0 < ntot; b0 += U * G::NTH) {
         float yv[U], wv[U];
-        int64_t off[U];
+        int off[U], so[U];
         bool ok[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int idx = b0 + tid + u * G::NTH;
-            const int rr = idx / T, cc = idx - rr * T;
-            const int oi = t.y0 + r0 + rr, oj = t.x0 + cc;
-            ok[u] = idx < ntot && oi < min(Fd.my, t.ylim) && oj < min(Fd.mx, t.xlim);
-            off[u] = (int64_t)oi * Fd.op + oj;
-            yv[u] = (ok[u] && mode != FFT_PLAIN) ? __ldg(Fd.y + off[u]) : 0.f;
-            wv[u] = (ok[u] && mode != FFT_PLAIN) ? (Fd.w ? __ldg(Fd.w + off[u]) : Fd.w_scalar) : 0.f;
+            ok[u] = b0 + tid + u * G::NTH < ntot;
+            off[u] = rr * Fd.op + cc;
+            so[u] = rr * XS + c2 + cc;
+            step();
+            yv[u] = (ok[u] && mode != FFT_PLAIN) ? __ldg(yb + off[u]) : 0.f;
+            wv[u] = (ok[u] && mode != FFT_PLAIN) ? (wb ? __ldg(wb + off[u]) : Fd.w_scalar) : 0.f;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (!ok[u]) continue;
-            const int idx = b0 + tid + u * G::NTH;
-            const int rr = idx / T, cc = idx - rr * T;
-            const float hx = outs[rr * XS + c2 + cc] * scale;
+            const float hx = outs[so[u]] * scale;
             if (mode == FFT_PLAIN) {
-                Fd.r[off[u]] = hx;
+                rb[off[u]] = hx;
             } else {
                 const float d = hx - yv[u];
-                if (mode == FFT_RESIDUAL) Fd.r[off[u]] = wv[u] * d;
+                if (mode == FFT_RESIDUAL) rb[off[u]] = wv[u] * d;
                 dsum += 0.5 * (double)wv[u] * (double)d * (double)d;
             }
         }

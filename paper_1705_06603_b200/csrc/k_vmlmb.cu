@@ -12,7 +12,7 @@
 namespace deblur {
 namespace {
 
-constexpr int VT_Y = 32, VT_X = 128, VNT = 256, VPT = VT_Y * VT_X / VNT;
+constexpr int VT_Y = 32, VT_X = 128, VNT = 256;
 
 __device__ __forceinline__ double block_sum3(double v, double *red, int which) {
     // one of up to three independent block sums (red holds 3 x 8 doubles)
