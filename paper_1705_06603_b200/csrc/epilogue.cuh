@@ -76,7 +76,7 @@ __device__ __forceinline__ float update_pixel(const FacetDev &F, const float *xh
 // psi_y(i-1,j) - psi_y(i,j) + psi_x(i,j-1) - psi_x(i,j)) and, if asked, phi(D x)(i, j).
 // Compile-time regulariser / D boundary (REG: 0 smoothed TV, 1 Huber; NEU: Neumann).
 template <int REG, bool NEU>
-__device__ __forceinline__ float tv_grad_t(const FacetDev &F, const float *xh, int XH, int i, int j, int fy, int fx,
+__device__ __forceinline__ float tv_grad_t(int ny, int nx, const float *xh, int XH, int i, int j, int fy, int fx,
                                            const SolverConst &sc, bool want_phi, float &phi) {
     const float e2 = sc.eps * sc.eps;
     auto X = [&](int a, int b) { return xh[a * XH + b]; };
@@ -88,7 +88,6 @@ __device__ __forceinline__ float tv_grad_t(const FacetDev &F, const float *xh, i
     float dyl = X(i + 1, j - 1) - X(i, j - 1);
     float dxl = xc - X(i, j - 1);
     if (NEU) {
-        const int ny = F.ny, nx = F.nx;
         const int fyu = (fy == 0) ? ny - 1 : fy - 1;
         const int fxl = (fx == 0) ? nx - 1 : fx - 1;
         if (fy == ny - 1) { dyc = 0.f; dyl = 0.f; }
@@ -116,16 +115,14 @@ __device__ __forceinline__ float tv_grad_t(const FacetDev &F, const float *xh, i
 }
 
 // Same arithmetic as update_pixel, returning x+ and the dual/band values instead of
-// storing them (the caller vectorises the stores); phi is computed only when asked.
+// storing them (the caller vectorises the stores and supplies omega^F at the pixel,
+// computed once per row and column); phi is computed only when asked.
 template <int REG, bool NEU>
-__device__ __forceinline__ float update_value_t(const FacetDev &F, const float *xh, int XH, int i, int j, int fy,
-                                                int fx, float g, float uc, const SolverConst &sc, bool want_phi,
-                                                float &phi, bool &shared, float &u_new, float &v_new) {
+__device__ __forceinline__ float update_value_t(int ny, int nx, const float *xh, int XH, int i, int j, int fy, int fx,
+                                                float g, float uc, float om, const SolverConst &sc, bool want_phi,
+                                                float &phi, float &u_new, float &v_new) {
     const float xc = xh[i * XH + j];
-    const float tdiv = tv_grad_t<REG, NEU>(F, xh, XH, i, j, fy, fx, sc, want_phi, phi);
-    shared = fy < F.ay.b_prev || fy >= F.ay.b_next || fx < F.ax.b_prev || fx >= F.ax.b_next;
-    // A13 ramps are 1 off the bands; per-node weights (F.ay.w) are not
-    const float om = (shared || F.ay.w) ? omega_axis(F.ay, fy) * omega_axis(F.ax, fx) : 1.f;
+    const float tdiv = tv_grad_t<REG, NEU>(ny, nx, xh, XH, i, j, fy, fx, sc, want_phi, phi);
     const float gt = g + sc.lambda * tdiv + sc.gamma * om * (xc - uc);
     const float xn = fmaxf(0.f, xc - sc.tau * gt);
     u_new = uc + sc.rho * (xn - uc);

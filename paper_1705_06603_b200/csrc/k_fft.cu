@@ -359,11 +359,12 @@ __global__ void __launch_bounds__(256) k_rows_fwd(FftArgs A, int mode, int par, 
     }
     for (int i = tid; i < ROWS_TW(S); i += G::NTH) Wsm[i] = A.W[i];
     {
-        // batched loads (all in flight before the first use): real rows of the window
-        constexpr int LPT = NB * S / G::NTH;
+        // batched loads (all in flight before the first use): real rows of the window;
+        // thread -> (row offset rt, column ct), the row / column bounds tested once each
+        constexpr int NTH = G::NTH, LPT = NB * S / NTH;
+        constexpr int CPR = S >= NTH ? S / NTH : 1, RPI = S >= NTH ? 1 : NTH / S;
         const float *src;
-        int64_t pitch;
-        int gy0, gx0, limy, limx;
+        int pitch, gy0, gx0, limy, limx;
         if (mode == 0) {
             src = Fd->x[par]; pitch = Fd->ep; gy0 = t.y0 + r0; gx0 = t.x0; limy = Fd->ny; limx = Fd->nx;
         } else if (mode == 1) {
@@ -371,24 +372,42 @@ __global__ void __launch_bounds__(256) k_rows_fwd(FftArgs A, int mode, int par, 
         } else {
             src = psfs + (int64_t)tile * P * P; pitch = P; gy0 = r0; gx0 = 0; limy = P; limx = P;
         }
+        const int ct = S >= NTH ? tid : tid % S, rt = S >= NTH ? 0 : tid / S;
+        const float *bp = src + (int64_t)(gy0 + rt) * pitch + gx0 + ct;
+        bool okx[CPR];
+#pragma unroll
+        for (int c = 0; c < CPR; ++c) okx[c] = gx0 + ct + c * NTH >= 0 && gx0 + ct + c * NTH < limx;
         float vals[LPT];
 #pragma unroll
         for (int it = 0; it < LPT; ++it) {
-            const int idx = tid + it * G::NTH, rr = idx / S, cc = idx % S;
-            const int gy = gy0 + rr, gx = gx0 + cc;
-            vals[it] = (gy >= 0 && gy < limy && gx >= 0 && gx < limx) ? __ldg(src + (int64_t)gy * pitch + gx) : 0.f;
+            const int ro = (it / CPR) * RPI, c = it % CPR, gy = gy0 + rt + ro;
+            vals[it] = (okx[c] && gy >= 0 && gy < limy) ? __ldg(bp + ro * pitch + c * NTH) : 0.f;
         }
 #pragma unroll
         for (int it = 0; it < LPT; ++it) {
-            const int idx = tid + it * G::NTH, rr = idx / S, cc = idx % S;
-            xs[rr * XS + cc] = vals[it];
+            const int ro = (it / CPR) * RPI, c = it % CPR;
+            xs[(rt + ro) * XS + ct + c * NTH] = vals[it];
         }
     }
+    // wx_q of the next active q in flight during this q's transform (mode 0)
+    constexpr int WPT = (S + G::NTH - 1) / G::NTH;
+    float wpre[WPT];
+    auto load_w = [&](int q) {
+        const float *wxq = A.wx + (size_t)q * A.Nx + Fd->ex0 + t.x0;
+#pragma unroll
+        for (int k = 0; k < WPT; ++k) {
+            const int i = tid + k * G::NTH;
+            wpre[k] = (i < S && t.x0 + i < Fd->nx) ? __ldg(wxq + i) : 0.f;
+        }
+    };
+    if (mode == 0 && nq > 0) load_w(q0);
     for (int qi = 0; qi < nq; ++qi) {
         if (mode == 0) {
-            __syncthreads();
-            const float *wxq = A.wx + (size_t)(q0 + qi) * A.Nx + Fd->ex0 + t.x0;
-            for (int i = tid; i < S; i += G::NTH) wxs[i] = (t.x0 + i < Fd->nx) ? __ldg(wxq + i) : 0.f;
+            // the previous q's stage-0 readers of wxs passed a barrier since
+#pragma unroll
+            for (int k = 0; k < WPT; ++k)
+                if (tid + k * G::NTH < S) wxs[tid + k * G::NTH] = wpre[k];
+            if (qi + 1 < nq) load_w(q0 + qi + 1);
         }
         __syncthreads();
         // stage 0 straight from the real rows: z[n] = (x[2n] w[2n], x[2n+1] w[2n+1])
@@ -1164,7 +1183,8 @@ __global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
     };
     if (ht) {
         float *gb = Fd.g + (int64_t)(t.y0 + r0) * Fd.ep + t.x0;
-        for (int idx = tid; idx < ntot; idx += G::NTH, step()) gb[rr * Fd.ep + cc] = outs[rr * XS + cc] * scale;
+        const int ep = (int)Fd.ep;
+        for (int idx = tid; idx < ntot; idx += G::NTH, step()) gb[rr * ep + cc] = outs[rr * XS + cc] * scale;
         return;
     }
     double dsum = 0.0;
@@ -1172,6 +1192,8 @@ __global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
     const int64_t obase = (int64_t)(t.y0 + r0) * Fd.op + t.x0;
     const float *yb = Fd.y + obase, *wb = Fd.w ? Fd.w + obase : nullptr;
     float *rb = Fd.r + obase;
+    const int op = (int)Fd.op;
+    const float w_scalar = Fd.w_scalar;
     for (int b0 = 0; b0 < ntot; b0 += U * G::NTH) {
         float yv[U], wv[U];
         int off[U], so[U];
@@ -1179,11 +1201,11 @@ __global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             ok[u] = b0 + tid + u * G::NTH < ntot;
-            off[u] = rr * Fd.op + cc;
+            off[u] = rr * op + cc;
             so[u] = rr * XS + c2 + cc;
             step();
             yv[u] = (ok[u] && mode != FFT_PLAIN) ? __ldg(yb + off[u]) : 0.f;
-            wv[u] = (ok[u] && mode != FFT_PLAIN) ? (wb ? __ldg(wb + off[u]) : Fd.w_scalar) : 0.f;
+            wv[u] = (ok[u] && mode != FFT_PLAIN) ? (wb ? __ldg(wb + off[u]) : w_scalar) : 0.f;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {

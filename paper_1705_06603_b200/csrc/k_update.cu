@@ -32,6 +32,10 @@ __global__ void __launch_bounds__(EPI_NT, K4_MINB) k_update_from_g(const FacetDe
     constexpr int XH = UT_TX + 8;                    // smem col c <-> facet col x0 - 4 + c
     __shared__ __align__(16) float xh[(UT_TY + 2) * XH];
     __shared__ double red[EPI_NT / 32];
+    __shared__ __align__(16) float om_c[UT_TX];
+    __shared__ float om_r[UT_TY];
+    __shared__ __align__(4) unsigned char sb_c[UT_TX];
+    __shared__ unsigned char sb_r[UT_TY];
     const TileDesc t = tiles[blockIdx.x];
     const FacetDev &F = facets[t.f];
     const float *__restrict__ x = F.x[par];
@@ -74,6 +78,17 @@ __global__ void __launch_bounds__(EPI_NT, K4_MINB) k_update_from_g(const FacetDe
             }
         }
     }
+    // band membership and omega^F (A13 ramps or per-node weights) once per tile column
+    // and row, into shared memory (in registers they would spill at 4 CTAs / SM)
+    if (tid < UT_TX) {
+        const int fx = t.x0 + tid;
+        om_c[tid] = fx < F.nx ? omega_axis(F.ax, fx) : 1.f;
+        sb_c[tid] = fx < F.ax.b_prev || fx >= F.ax.b_next;
+    } else if (tid < UT_TX + UT_TY) {
+        const int fy = t.y0 + tid - UT_TX;
+        om_r[tid - UT_TX] = fy < F.ny ? omega_axis(F.ay, fy) : 1.f;
+        sb_r[tid - UT_TX] = fy < F.ay.b_prev || fy >= F.ay.b_next;
+    }
     if (!interior) {
         for (int idx = tid; idx < (UT_TY + 2) * XH; idx += EPI_NT) {
             const int i = idx / XH, c = idx - i * XH;
@@ -93,14 +108,21 @@ __global__ void __launch_bounds__(EPI_NT, K4_MINB) k_update_from_g(const FacetDe
         const int fy = t.y0 + ly;
         if (fy >= F.ny || fx0 >= F.nx) continue;
         const int64_t o = (int64_t)fy * F.ep + fx0;
+        const bool shy = sb_r[ly];
+        const float omy = om_r[ly];
+        const float4 omx = *reinterpret_cast<const float4 *>(om_c + lx0);
+        const uchar4 shx = *reinterpret_cast<const uchar4 *>(sb_c + lx0);
+        const float omxj[4] = {omx.x, omx.y, omx.z, omx.w};
+        const bool shxj[4] = {shx.x != 0, shx.y != 0, shx.z != 0, shx.w != 0};
         float xn[4], nu[4], nv[4];
         bool sh[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int fx = fx0 + j;
             float phi;
-            xn[j] = update_value_t<REG, NEU>(F, xh, XH, ly + 1, lx0 + j + 4, fy, fx, gv[k][j], uv[k][j], sc,
-                                             partials != nullptr, phi, sh[j], nu[j], nv[j]);
+            sh[j] = shy || shxj[j];
+            xn[j] = update_value_t<REG, NEU>(F.ny, F.nx, xh, XH, ly + 1, lx0 + j + 4, fy, fx, gv[k][j], uv[k][j],
+                                             omy * omxj[j], sc, partials != nullptr, phi, nu[j], nv[j]);
             if (fx < F.nx) rsum += (double)phi;
         }
         if (full) {

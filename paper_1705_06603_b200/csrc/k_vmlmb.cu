@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(VNT) k_grad(VmArgs a, SolverConst sc) {
         const int64_t o = o4 + jj;
         const int ly = fy - t.y0, lx = fx - t.x0;
         float phi;
-        const float tdiv = tv_grad_t<REG, NEU>(F, xh, XH, ly + 1, lx + 4, fy, fx, sc, true, phi);
+        const float tdiv = tv_grad_t<REG, NEU>(F.ny, F.nx, xh, XH, ly + 1, lx + 4, fy, fx, sc, true, phi);
         const float xc = xh[(ly + 1) * XH + lx + 4], uc = F.u[o];
         const bool shared = fy < F.ay.b_prev || fy >= F.ay.b_next || fx < F.ax.b_prev || fx >= F.ax.b_next;
         const float om = (shared || F.ay.w) ? omega_axis(F.ay, fy) * omega_axis(F.ax, fx) : 1.f;
