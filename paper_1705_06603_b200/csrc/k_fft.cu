@@ -48,6 +48,9 @@
 #ifndef COLS_TM_NB
 #define COLS_TM_NB 8
 #endif
+#ifndef COLS_TM_TWTMEM
+#define COLS_TM_TWTMEM 1   // per-thread twiddles of the TMEM column pass in TMEM
+#endif
 #ifndef COLS_TM_MINB
 #define COLS_TM_MINB (16 / COLS_TM_NB)
 #endif
@@ -157,6 +160,31 @@ __host__ __device__ constexpr int fft_rad(int L, int s) {
 }
 __host__ __device__ constexpr int fft_ns(int L, int s) { return s == 0 ? 1 : fft_ns(L, s - 1) * fft_rad(L, s - 1); }
 
+// Twiddle providers for the stages with Ns > 1: get<Ns, R>(i, j, w) fills w[1..R-1] =
+// W_L^{r k}, k = j % Ns, for butterfly j (the thread's i-th of the stage).
+// TwTable: w, w^2, w^4 from the fp64-built table in shared memory, the rest by at most
+// two products (<= ~2 ulp), saving shared-memory loads.
+struct TwTable {
+    const float2 *W;
+    int S;
+    template <int Ns, int R>
+    __device__ __forceinline__ void get(int, int j, float2 (&w)[8]) const {
+        const int k = j % Ns;
+        const int step = S / (Ns * R);
+        w[1] = W[(k * step) & (S - 1)];
+        if (R >= 4) {
+            w[2] = W[(2 * k * step) & (S - 1)];
+            w[3] = cmul(w[1], w[2]);
+        }
+        if (R == 8) {
+            w[4] = W[(4 * k * step) & (S - 1)];
+            w[5] = cmul(w[4], w[1]);
+            w[6] = cmul(w[4], w[2]);
+            w[7] = cmul(w[4], w[3]);
+        }
+    }
+};
+
 // One Stockham stage of NB batched length-L transforms at buf[t*STRIDE + n] executed
 // by NTH threads.  Thread tid owns transform t = tid % NB (transform-fastest: a
 // quarter-/half-warp touches 8/16 transforms at one position, which the padded
@@ -177,26 +205,11 @@ struct Stage {
     }
     __device__ static __forceinline__ int in_n(int j, int r) { return j + r * LR; }
     __device__ static __forceinline__ int out_n(int j, int r) { return (j / Ns) * Ns * R + (j % Ns) + r * Ns; }
-    template <int SIGN>
-    __device__ static __forceinline__ void bfly(float2 *v, int j, const float2 *W, int S) {
+    template <int SIGN, class TW>
+    __device__ static __forceinline__ void bfly_tw(float2 *v, int i, int j, const TW &tw) {
         if (Ns > 1) {
-            // w^r for r = 1..R-1: w, w^2, w^4 from the fp64-built table, the rest by at
-            // most two products (<= ~2 ulp), saving shared-memory loads (the column pass
-            // is bound by shared-memory wavefronts)
-            const int k = j % Ns;
-            const int step = S / (Ns * R);
             float2 w[8];
-            w[1] = W[(k * step) & (S - 1)];
-            if (R >= 4) {
-                w[2] = W[(2 * k * step) & (S - 1)];
-                w[3] = cmul(w[1], w[2]);
-            }
-            if (R == 8) {
-                w[4] = W[(4 * k * step) & (S - 1)];
-                w[5] = cmul(w[4], w[1]);
-                w[6] = cmul(w[4], w[2]);
-                w[7] = cmul(w[4], w[3]);
-            }
+            tw.template get<Ns, R>(i, j, w);
 #pragma unroll
             for (int r = 1; r < R; ++r) {
                 float2 ww = w[r];
@@ -209,7 +222,11 @@ struct Stage {
         else dft2<SIGN>(v[0], v[1]);
     }
     template <int SIGN>
-    __device__ static __forceinline__ void load_bfly(const float2 *buf, float2 (&v)[E], int tid, const float2 *W, int S) {
+    __device__ static __forceinline__ void bfly(float2 *v, int j, const float2 *W, int S) {
+        bfly_tw<SIGN>(v, 0, j, TwTable{W, S});
+    }
+    template <int SIGN, class TW>
+    __device__ static __forceinline__ void load_bfly_tw(const float2 *buf, float2 (&v)[E], int tid, const TW &tw) {
         if constexpr (VEC) {
             // butterflies (i, i+1) read the adjacent positions (n, n+1)
 #pragma unroll
@@ -222,8 +239,8 @@ struct Stage {
                     v[i * R + r] = make_float2(q.x, q.y);
                     v[(i + 1) * R + r] = make_float2(q.z, q.w);
                 }
-                bfly<SIGN>(&v[i * R], j, W, S);
-                bfly<SIGN>(&v[(i + 1) * R], j + 1, W, S);
+                bfly_tw<SIGN>(&v[i * R], i, j, tw);
+                bfly_tw<SIGN>(&v[(i + 1) * R], i + 1, j + 1, tw);
             }
         } else {
 #pragma unroll
@@ -232,9 +249,13 @@ struct Stage {
                 bj(i, tid, t, j);
 #pragma unroll
                 for (int r = 0; r < R; ++r) v[i * R + r] = buf[t * STRIDE + in_n(j, r)];
-                bfly<SIGN>(&v[i * R], j, W, S);
+                bfly_tw<SIGN>(&v[i * R], i, j, tw);
             }
         }
+    }
+    template <int SIGN>
+    __device__ static __forceinline__ void load_bfly(const float2 *buf, float2 (&v)[E], int tid, const float2 *W, int S) {
+        load_bfly_tw<SIGN>(buf, v, tid, TwTable{W, S});
     }
     __device__ static __forceinline__ void store(float2 *buf, const float2 (&v)[E], int tid) {
         if constexpr (VEC && Ns == 1) {
@@ -278,18 +299,20 @@ struct Stage {
 template <int L, int NB, int STRIDE, int NTH, int SIGN, int s, int NS>
 struct Mid {
     static constexpr int E = NB * L / NTH;
-    __device__ static __forceinline__ void run(float2 *work, float2 (&v)[E], int tid, const float2 *W, int S) {
+    template <class TW>
+    __device__ static __forceinline__ void run(float2 *work, float2 (&v)[E], int tid, const TW &tw) {
         Stage<L, NB, STRIDE, NTH, s - 1>::store(work, v, tid);
         __syncthreads();
-        Stage<L, NB, STRIDE, NTH, s>::template load_bfly<SIGN>(work, v, tid, W, S);
+        Stage<L, NB, STRIDE, NTH, s>::template load_bfly_tw<SIGN>(work, v, tid, tw);
         __syncthreads();
-        Mid<L, NB, STRIDE, NTH, SIGN, s + 1, NS>::run(work, v, tid, W, S);
+        Mid<L, NB, STRIDE, NTH, SIGN, s + 1, NS>::run(work, v, tid, tw);
     }
 };
 template <int L, int NB, int STRIDE, int NTH, int SIGN, int NS>
 struct Mid<L, NB, STRIDE, NTH, SIGN, NS, NS> {
     static constexpr int E = NB * L / NTH;
-    __device__ static __forceinline__ void run(float2 *, float2 (&)[E], int, const float2 *, int) {}
+    template <class TW>
+    __device__ static __forceinline__ void run(float2 *, float2 (&)[E], int, const TW &) {}
 };
 
 template <int L, int NB, int STRIDE, int NTH>
@@ -300,7 +323,11 @@ struct Fft {
     using Last = Stage<L, NB, STRIDE, NTH, NS - 1>;
     template <int SIGN>
     __device__ static __forceinline__ void middle(float2 *work, float2 (&v)[E], int tid, const float2 *W, int S) {
-        Mid<L, NB, STRIDE, NTH, SIGN, 1, NS>::run(work, v, tid, W, S);
+        Mid<L, NB, STRIDE, NTH, SIGN, 1, NS>::run(work, v, tid, TwTable{W, S});
+    }
+    template <int SIGN, class TW>
+    __device__ static __forceinline__ void middle_tw(float2 *work, float2 (&v)[E], int tid, const TW &tw) {
+        Mid<L, NB, STRIDE, NTH, SIGN, 1, NS>::run(work, v, tid, tw);
     }
 };
 
@@ -785,13 +812,34 @@ __device__ __forceinline__ void tm_get(uint32_t ta, float2 (&v)[E]) {
     for (int e = 0; e < E; ++e) v[e] = make_float2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
 }
 
+// Twiddle provider of the TMEM column pass (S = 512, stages 1 and 2 with Ns = 8, 64, two
+// butterflies per thread each): w^1..w^7 of the thread's butterfly i of that stage in 16
+// TMEM columns at base + (slot * 2 + i) * 16, written once per CTA from TwTable (same
+// values), so a transform reads one tcgen05.ld per butterfly instead of 3 shared loads and
+// 4 complex products.
+struct TwTmem {
+    uint32_t base;
+    template <int Ns, int R>
+    __device__ __forceinline__ void get(int i, int, float2 (&w)[8]) const {
+        static_assert(R == 8 && (Ns == 8 || Ns == 64), "512-point radix-8 plan");
+        constexpr int slot = Ns == 8 ? 0 : 1;
+        uint32_t r[16];
+        tm_ld16(base + (uint32_t)((slot * 2 + i) * 16), r);
+        tm_wait_ld();
+#pragma unroll
+        for (int k = 1; k < 8; ++k) w[k] = make_float2(__uint_as_float(r[2 * k - 2]), __uint_as_float(r[2 * k - 1]));
+    }
+};
+
 template <int S>
 struct GCT {
     // NB columns per CTA with NTH = 32 NB threads: 16 elements per thread at S = 512;
     // CS = S + 16/NB makes the paired 16-byte exchanges conflict-free per quarter-warp
     static constexpr int NB = COLS_TM_NB, NTH = 32 * NB, CS = S + 16 / NB;
     static constexpr int E = NB * S / NTH;
-    static constexpr int TMCOLS = NB >= 8 ? 64 * (NB / 4) : 64;   // 4 lane quarters x (NB/4 warps x 64 columns)
+    // per warp: 32 input + 32 accumulator columns (+ 64 twiddle columns); 4 lane quarters x NB/4 warps
+    static constexpr int WCOLS = COLS_TM_TWTMEM ? 128 : 64;
+    static constexpr int TMCOLS = NB >= 8 ? WCOLS * (NB / 4) : WCOLS;
     using F = Fft<S, NB, CS, NTH>;
 };
 template <int S>
@@ -845,8 +893,36 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     // this thread's TMEM lane (warp quarter) and its 64 columns: [0, 32) inputs, [32, 64) accumulator
-    const uint32_t t_in = *tm_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 64);
+    const uint32_t t_in = *tm_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * G::WCOLS);
     const uint32_t t_acc = t_in + 32;
+#if COLS_TM_TWTMEM
+    {
+        using S1 = Stage<S, NB, CS, NTH, 1>;
+        using S2 = Stage<S, NB, CS, NTH, 2>;
+        static_assert(F::NS == 3 && S1::R == 8 && S2::R == 8 && S1::BPT == 2 && S2::BPT == 2, "twiddle slots");
+        const TwTable tt{Wsm, S};
+#pragma unroll
+        for (int slot = 0; slot < 2; ++slot) {
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                int t, j;
+                S1::bj(i, tid, t, j);
+                float2 w[8];
+                if (slot == 0) tt.get<S1::Ns, 8>(i, j, w);
+                else tt.get<S2::Ns, 8>(i, j, w);
+                uint32_t r[16];
+#pragma unroll
+                for (int k = 1; k < 8; ++k) { r[2 * k - 2] = __float_as_uint(w[k].x); r[2 * k - 1] = __float_as_uint(w[k].y); }
+                r[14] = r[15] = 0u;
+                tm_st16(t_acc + 32 + (uint32_t)((slot * 2 + i) * 16), r);
+            }
+        }
+        tm_wait_st();
+    }
+    const TwTmem tw{t_acc + 32};
+#else
+    const TwTable tw{Wsm, S};
+#endif
     const int nqt = td.q1 - td.q0 + 1;
     auto hk = [&](int p, int q) { return A.Hhat + (int64_t)slot_s[(p - td.p0) * nqt + (q - td.q0)] * S * LDF; };
     // stage-0 input positions of this thread, straight from the global chunk (row stride LDF)
@@ -886,7 +962,7 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
                     S0::template bfly<-1>(&v[i * S0::R], j, Wsm, S);
                     S0::template bfly<-1>(&v[(i + 1) * S0::R], j + 1, Wsm, S);
                 }
-                F::template middle<-1>(work, v, tid, Wsm, S);
+                F::template middle_tw<-1>(work, v, tid, tw);
                 __pipeline_wait_prior(0);
                 __syncthreads();                   // Hhat chunk visible
                 // acc += v . Hhat, in two halves of 8 complex (16 TMEM columns each)
@@ -932,7 +1008,7 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
             S0::template bfly<+1>(&v[i * S0::R], j, Wsm, S);
         }
         __syncthreads();
-        F::template middle<+1>(work, v, tid, Wsm, S);
+        F::template middle_tw<+1>(work, v, tid, tw);
         float2 *O = base + (int64_t)A.NQ * S * LDF + f0;
 #pragma unroll
         for (int i = 0; i < SL::BPT; ++i) {
@@ -954,7 +1030,7 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
             S0::bj(i, tid, t, j);
             S0::template bfly<-1>(&v[i * S0::R], j, Wsm, S);
         }
-        F::template middle<-1>(work, v, tid, Wsm, S);
+        F::template middle_tw<-1>(work, v, tid, tw);
         tm_put<E>(t_in, v);                        // last-stage positions == stage-0 positions
         tm_wait_st();
         float2 *Bbase = base + (int64_t)S * LDF + f0;
@@ -984,7 +1060,7 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
                     if (np > td.p1) { np = td.p0; ++nq; }
                     if (nq <= td.q1) prefetch_hhat<S, NB, NTH, LDF>(hbuf, hk(np, nq), f0, tid);
                 }
-                F::template middle<+1>(work, v, tid, Wsm, S);
+                F::template middle_tw<+1>(work, v, tid, tw);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     uint32_t a[16];
