@@ -1188,14 +1188,18 @@ __global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
     auto src = [&](int qi) {
         return ht ? Bbase + ((int64_t)qi * T + r0) * LDF : base + ((int64_t)A.NQ * S + r0) * LDF;
     };
-    if (nq > 0) C::issue(stg, src(0), nrows, tid);
-    for (int i = tid; i < ROWS_TW(S); i += G::NTH) Wsm[i] = A.W[i];
     if (ht) {
+        // wx_q rows of all active q: cp.async, committed with the first staging group below
         for (int idx = tid; idx < nq * S; idx += G::NTH) {
             const int qi = idx / S, cc = idx - qi * S;
-            wxs[idx] = (cc < T && t.x0 + cc < Fd.nx) ? __ldg(A.wx + (size_t)(t.q0 + qi) * A.Nx + Fd.ex0 + t.x0 + cc) : 0.f;
+            if (cc < T && t.x0 + cc < Fd.nx)
+                __pipeline_memcpy_async(wxs + idx, A.wx + (size_t)(t.q0 + qi) * A.Nx + Fd.ex0 + t.x0 + cc, 4);
+            else
+                wxs[idx] = 0.f;
         }
     }
+    if (nq > 0) C::issue(stg, src(0), nrows, tid);
+    for (int i = tid; i < ROWS_TW(S); i += G::NTH) Wsm[i] = A.W[i];
     float2 acc[HT ? E : 1];
 #pragma unroll
     for (int e = 0; e < (HT ? E : 1); ++e) acc[e] = make_float2(0.f, 0.f);
@@ -1260,7 +1264,20 @@ __global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
     if (ht) {
         float *gb = Fd.g + (int64_t)(t.y0 + r0) * Fd.ep + t.x0;
         const int ep = (int)Fd.ep;
-        for (int idx = tid; idx < ntot; idx += G::NTH, step()) gb[rr * ep + cc] = outs[rr * XS + cc] * scale;
+        if (((t.x0 | nc | ep) & 1) == 0 && ((uintptr_t)gb & 7) == 0) {
+            // column pairs (8-byte aligned; XS even)
+            const int ncp = nc >> 1, ntp = nr * ncp, dr2 = G::NTH / ncp, dc2 = G::NTH - dr2 * ncp;
+            int r2 = tid / ncp, c2p = tid - r2 * ncp;
+            for (int idx = tid; idx < ntp; idx += G::NTH) {
+                const float2 o = *reinterpret_cast<const float2 *>(outs + r2 * XS + 2 * c2p);
+                *reinterpret_cast<float2 *>(gb + r2 * ep + 2 * c2p) = make_float2(o.x * scale, o.y * scale);
+                r2 += dr2;
+                c2p += dc2;
+                if (c2p >= ncp) { c2p -= ncp; ++r2; }
+            }
+        } else {
+            for (int idx = tid; idx < ntot; idx += G::NTH, step()) gb[rr * ep + cc] = outs[rr * XS + cc] * scale;
+        }
         return;
     }
     double dsum = 0.0;
@@ -1270,6 +1287,45 @@ __global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
     float *rb = Fd.r + obase;
     const int op = (int)Fd.op;
     const float w_scalar = Fd.w_scalar;
+    if (((t.x0 | nc | op | c2) & 1) == 0 && (((uintptr_t)yb | (uintptr_t)wb | (uintptr_t)rb) & 7) == 0) {
+        // column pairs: 8-byte loads / stores (same per-element arithmetic)
+        constexpr int U2 = U / 2;
+        const int ncp = nc >> 1, ntp = nr * ncp, dr2 = G::NTH / ncp, dc2 = G::NTH - dr2 * ncp;
+        int r2 = tid / ncp, cp = tid - r2 * ncp;
+        for (int b0 = 0; b0 < ntp; b0 += U2 * G::NTH) {
+            float2 yv[U2], wv[U2];
+            int off[U2], so[U2];
+            bool ok[U2];
+#pragma unroll
+            for (int u = 0; u < U2; ++u) {
+                ok[u] = b0 + tid + u * G::NTH < ntp;
+                off[u] = r2 * op + 2 * cp;
+                so[u] = r2 * XS + c2 + 2 * cp;
+                r2 += dr2;
+                cp += dc2;
+                if (cp >= ncp) { cp -= ncp; ++r2; }
+                const bool ld = ok[u] && mode != FFT_PLAIN;
+                yv[u] = ld ? __ldg(reinterpret_cast<const float2 *>(yb + off[u])) : make_float2(0.f, 0.f);
+                wv[u] = ld ? (wb ? __ldg(reinterpret_cast<const float2 *>(wb + off[u])) : make_float2(w_scalar, w_scalar))
+                           : make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < U2; ++u) {
+                if (!ok[u]) continue;
+                const float2 o = *reinterpret_cast<const float2 *>(outs + so[u]);
+                const float hx0 = o.x * scale, hx1 = o.y * scale;
+                float2 *rp = reinterpret_cast<float2 *>(rb + off[u]);
+                if (mode == FFT_PLAIN) {
+                    *rp = make_float2(hx0, hx1);
+                } else {
+                    const float d0 = hx0 - yv[u].x, d1 = hx1 - yv[u].y;
+                    if (mode == FFT_RESIDUAL) *rp = make_float2(wv[u].x * d0, wv[u].y * d1);
+                    dsum += 0.5 * (double)wv[u].x * (double)d0 * (double)d0;
+                    dsum += 0.5 * (double)wv[u].y * (double)d1 * (double)d1;
+                }
+            }
+        }
+    } else
     for (int b0 = 0; b0 < ntot; b0 += U * G::NTH) {
         float yv[U], wv[U];
         int off[U], so[U];
