@@ -399,21 +399,51 @@ __global__ void __launch_bounds__(256) k_rows_fwd(FftArgs A, int mode, int par, 
         } else {
             src = psfs + (int64_t)tile * P * P; pitch = P; gy0 = r0; gx0 = 0; limy = P; limx = P;
         }
-        const int ct = S >= NTH ? tid : tid % S, rt = S >= NTH ? 0 : tid / S;
-        const float *bp = src + (int64_t)(gy0 + rt) * pitch + gx0 + ct;
-        bool okx[CPR];
+        if (((gx0 | pitch) & 1) == 0 && ((uintptr_t)src & 7) == 0) {
+            // column pairs: 8-byte loads (a pair straddling the right edge is loaded per element)
+            constexpr int SP = S / 2, LP = LPT / 2;
+            constexpr int CP2 = SP >= NTH ? SP / NTH : 1, RP2 = SP >= NTH ? 1 : NTH / SP;
+            const int ct = SP >= NTH ? tid : tid % SP, rt = SP >= NTH ? 0 : tid / SP;
+            const float *bp = src + (int64_t)(gy0 + rt) * pitch + gx0 + 2 * ct;
+            int okx[CP2];      // 2: both columns in range, 1: the first only, 0: none
 #pragma unroll
-        for (int c = 0; c < CPR; ++c) okx[c] = gx0 + ct + c * NTH >= 0 && gx0 + ct + c * NTH < limx;
-        float vals[LPT];
+            for (int c = 0; c < CP2; ++c) {
+                const int gx = gx0 + 2 * (ct + c * NTH);
+                okx[c] = (gx >= 0 && gx < limx) + (gx + 1 >= 0 && gx + 1 < limx);
+            }
+            float2 vals[LP];
 #pragma unroll
-        for (int it = 0; it < LPT; ++it) {
-            const int ro = (it / CPR) * RPI, c = it % CPR, gy = gy0 + rt + ro;
-            vals[it] = (okx[c] && gy >= 0 && gy < limy) ? __ldg(bp + ro * pitch + c * NTH) : 0.f;
-        }
+            for (int it = 0; it < LP; ++it) {
+                const int ro = (it / CP2) * RP2, c = it % CP2, gy = gy0 + rt + ro;
+                const float *pp = bp + ro * pitch + 2 * c * NTH;
+                vals[it] = make_float2(0.f, 0.f);
+                if (gy >= 0 && gy < limy) {
+                    if (okx[c] == 2) vals[it] = __ldg(reinterpret_cast<const float2 *>(pp));
+                    else if (okx[c] == 1) vals[it].x = __ldg(pp);
+                }
+            }
 #pragma unroll
-        for (int it = 0; it < LPT; ++it) {
-            const int ro = (it / CPR) * RPI, c = it % CPR;
-            xs[(rt + ro) * XS + ct + c * NTH] = vals[it];
+            for (int it = 0; it < LP; ++it) {
+                const int ro = (it / CP2) * RP2, c = it % CP2;
+                *reinterpret_cast<float2 *>(xs + (rt + ro) * XS + 2 * (ct + c * NTH)) = vals[it];
+            }
+        } else {
+            const int ct = S >= NTH ? tid : tid % S, rt = S >= NTH ? 0 : tid / S;
+            const float *bp = src + (int64_t)(gy0 + rt) * pitch + gx0 + ct;
+            bool okx[CPR];
+#pragma unroll
+            for (int c = 0; c < CPR; ++c) okx[c] = gx0 + ct + c * NTH >= 0 && gx0 + ct + c * NTH < limx;
+            float vals[LPT];
+#pragma unroll
+            for (int it = 0; it < LPT; ++it) {
+                const int ro = (it / CPR) * RPI, c = it % CPR, gy = gy0 + rt + ro;
+                vals[it] = (okx[c] && gy >= 0 && gy < limy) ? __ldg(bp + ro * pitch + c * NTH) : 0.f;
+            }
+#pragma unroll
+            for (int it = 0; it < LPT; ++it) {
+                const int ro = (it / CPR) * RPI, c = it % CPR;
+                xs[(rt + ro) * XS + ct + c * NTH] = vals[it];
+            }
         }
     }
     // wx_q of the next active q in flight during this q's transform (mode 0)
