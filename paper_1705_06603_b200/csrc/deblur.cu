@@ -729,7 +729,7 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
                                  a == 0 ? -1 : 0, a == 2 ? 1 : 0, b == 0 ? -1 : 0, b == 2 ? 1 : 0};
                 const int ri = (int)h->rects.size();
                 h->rects.push_back(R);
-                for (int y = R.y0; y < R.y1; y += 8)
+                for (int y = R.y0; y < R.y1; y += CT_ROWS)
                     for (int x = R.x0; x < R.x1; x += 256) h->rect_tiles.push_back({ri, y, x});
             }
     }

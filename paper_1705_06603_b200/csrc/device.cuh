@@ -80,7 +80,8 @@ struct BandRect {         // consensus work item: facet-local rectangle of band 
     int dy0, dy1, dx0, dx1;   // the neighbour offsets contributing on the whole rectangle
 };
 
-struct RectTile {         // consensus launch unit: 8 rows x 256 columns of one BandRect
+constexpr int CT_ROWS = 32;   // rows of a consensus launch unit
+struct RectTile {         // consensus launch unit: CT_ROWS rows x 256 columns of one BandRect
     int rect, y0, x0;
 };
 

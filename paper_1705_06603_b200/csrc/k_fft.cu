@@ -1154,17 +1154,19 @@ struct C2R {
     // rows [0, nrows) of src0 -> stg (16-byte cp.async; rows >= nrows zero-filled)
     __device__ static __forceinline__ void issue(float2 *stg, const float2 *src0, int nrows, int tid) {
         constexpr int V = SH / 2;                 // 16-byte vectors per row, + the Nyquist element
-        for (int idx = tid; idx < NB * (V + 1); idx += G::NTH) {
-            const int rr = idx / (V + 1), v = idx - rr * (V + 1);
+        static_assert(V % 2 == 0 || V == 1, "row split");
+        // the 16-byte vectors of NB rows, row-major, by a power-of-two index split (no division)
+        for (int idx = tid; idx < NB * V; idx += G::NTH) {
+            const int rr = idx / V, v = idx % V;
             float2 *d = stg + rr * SS + 2 * v;
-            if (rr < nrows) {
-                const float2 *sp = src0 + (int64_t)rr * LDF + 2 * v;
-                if (v < V) __pipeline_memcpy_async(d, sp, 16);
-                else __pipeline_memcpy_async(d, sp, 8);
-            } else {
-                d[0] = make_float2(0.f, 0.f);
-                if (v < V) d[1] = make_float2(0.f, 0.f);
-            }
+            if (rr < nrows) __pipeline_memcpy_async(d, src0 + (int64_t)rr * LDF + 2 * v, 16);
+            else *reinterpret_cast<float4 *>(d) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        // the Nyquist element of each row
+        for (int rr = tid; rr < NB; rr += G::NTH) {
+            float2 *d = stg + rr * SS + SH;
+            if (rr < nrows) __pipeline_memcpy_async(d, src0 + (int64_t)rr * LDF + SH, 8);
+            else d[0] = make_float2(0.f, 0.f);
         }
         __pipeline_commit();
     }

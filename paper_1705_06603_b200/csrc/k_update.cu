@@ -187,25 +187,32 @@ __device__ __forceinline__ float view_at(const View &v, int par, int gy, int gx)
     return v.base[par][(int64_t)(gy - v.y0) * v.pitch + (gx - v.x0)];
 }
 
-// one CTA per RectTile (8 rows x 256 columns of a band piece).  The contributing
+// one CTA per RectTile (CT_ROWS rows x 256 columns of a band piece).  The contributing
 // neighbour offsets are constant on the piece: their descriptors (v pointer at this
-// column, pitch, omega along x) and the 8 rows' omega along y are resolved once per
-// thread, so the row loop is loads + arithmetic only.
+// column, pitch, omega along x) are resolved once per thread and the rows' omega along
+// y once per CTA (shared memory), so the row loop is loads + arithmetic only.
 __global__ void __launch_bounds__(256) k_consensus(const FacetDev *facets, const BandRect *rects,
                                                    const RectTile *tiles, int par, float rho) {
+    __shared__ float omy_s[2][CT_ROWS];
     const RectTile T = tiles[blockIdx.x];
     const BandRect R = rects[T.rect];
     const FacetDev &F = facets[R.f];
+    const int gy0 = F.ey0 + T.y0;
+    const int nr = min(CT_ROWS, R.y1 - T.y0);
+    if (threadIdx.x < 2 * CT_ROWS) {
+        const int a = threadIdx.x / CT_ROWS, r = threadIdx.x % CT_ROWS;
+        const int dy = R.dy0 + a;
+        const Neighbour &nb = F.nb[min(dy, 1) + 1][R.dx0 + 1];
+        omy_s[a][r] = (dy <= R.dy1 && r < nr) ? omega_axis(nb.ay, gy0 + r - nb.ay.e0) : 0.f;
+    }
+    __syncthreads();
     const int lx = T.x0 + (int)threadIdx.x;
     if (lx >= R.x1) return;
     const int gx = F.ex0 + lx;
-    const int gy0 = F.ey0 + T.y0;
-    const int nr = min(8, R.y1 - T.y0);
     const int ndx = R.dx1 - R.dx0 + 1, nc = (R.dy1 - R.dy0 + 1) * ndx;
     const float *vp[4];
     int64_t vpitch[4];
     float omx[4];
-    float omy[2][8];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
         vp[c] = nullptr; vpitch[c] = 0; omx[c] = 0.f;
@@ -217,41 +224,37 @@ __global__ void __launch_bounds__(256) k_consensus(const FacetDev *facets, const
             omx[c] = omega_axis(nb.ax, gx - nb.ax.e0);
         }
     }
+    const int64_t ep = F.ep;
+    float *__restrict__ up = F.u + (int64_t)T.y0 * ep + lx;
+    const float *__restrict__ xp = F.x[par] + (int64_t)T.y0 * ep + lx;
+    for (int g = 0; g < nr; g += 8) {
+        // every load of 8 rows in flight before the first use (v / x through the
+        // read-only path: the u stores cannot alias them)
+        float vv[8][4], xv[8], uv[8];
 #pragma unroll
-    for (int a = 0; a < 2; ++a) {
-        const int dy = R.dy0 + a;
-        const Neighbour &nb = F.nb[min(dy, 1) + 1][R.dx0 + 1];
+        for (int r = 0; r < 8; ++r) {
+            const bool ok = g + r < nr;
+            const int64_t rr = g + r;
 #pragma unroll
-        for (int r = 0; r < 8; ++r)
-            omy[a][r] = (dy <= R.dy1 && r < nr) ? omega_axis(nb.ay, gy0 + r - nb.ay.e0) : 0.f;
-    }
-    float *__restrict__ up = F.u + (int64_t)T.y0 * F.ep + lx;
-    const float *__restrict__ xp = F.x[par] + (int64_t)T.y0 * F.ep + lx;
-    // every load of the 8 rows in flight before the first use (v / x through the
-    // read-only path: the u stores cannot alias them)
-    float vv[8][4], xv[8], uv[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-        const bool ok = r < nr;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) vv[r][c] = (ok && c < nc) ? __ldg(vp[c] + (int64_t)r * vpitch[c]) : 0.f;
-        xv[r] = ok ? __ldg(xp + (int64_t)r * F.ep) : 0.f;
-        uv[r] = ok ? up[(int64_t)r * F.ep] : 0.f;
-    }
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-        if (r >= nr) break;
-        float num = 0.f, den = 0.f;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            if (c < nc) {
-                const float om = omy[c / ndx][r] * omx[c];
-                num += om * vv[r][c];
-                den += om;
-            }
+            for (int c = 0; c < 4; ++c) vv[r][c] = (ok && c < nc) ? __ldg(vp[c] + rr * vpitch[c]) : 0.f;
+            xv[r] = ok ? __ldg(xp + rr * ep) : 0.f;
+            uv[r] = ok ? up[rr * ep] : 0.f;
         }
-        const float zbar = num / den;
-        up[(int64_t)r * F.ep] = uv[r] + rho * (zbar - xv[r]);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            if (g + r >= nr) break;
+            float num = 0.f, den = 0.f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                if (c < nc) {
+                    const float om = omy_s[c / ndx][g + r] * omx[c];
+                    num += om * vv[r][c];
+                    den += om;
+                }
+            }
+            const float zbar = num / den;
+            up[(int64_t)(g + r) * ep] = uv[r] + rho * (zbar - xv[r]);
+        }
     }
 }
 
