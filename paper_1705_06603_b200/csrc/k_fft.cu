@@ -85,18 +85,22 @@ __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
-// R2C post step for bin k from Z_k, Z_{SH-k} and W_S^k: (Z_k + Z*_{SH-k})/2 - i/2 W^k (Z_k - Z*_{SH-k})
+// The R2C post step and the C2R pre step omit their factors 1/2: every spectrum between
+// the passes (and the PSF spectra) is 2x the DFT, and the C2R output 8x the operator's
+// value; the epilogue scale absorbs the 1/8 (FftArgs::scale).  Powers of two are exact,
+// so the results are bit-identical to the textbook form.
+// R2C post step for bin k from Z_k, Z_{SH-k} and W_S^k: 2 X_k = (Z_k + Z*_{SH-k}) - i W^k (Z_k - Z*_{SH-k})
 __device__ __forceinline__ float2 r2c_post(float2 zk, float2 zp, float2 w) {
-    const float2 sh = make_float2(0.5f * (zk.x + zp.x), 0.5f * (zk.y - zp.y));
-    const float2 d = make_float2(0.5f * (zk.x - zp.x), 0.5f * (zk.y + zp.y));
+    const float2 sh = make_float2(zk.x + zp.x, zk.y - zp.y);
+    const float2 d = make_float2(zk.x - zp.x, zk.y + zp.y);
     const float2 wd = cmul(w, d);
     return make_float2(sh.x + wd.y, sh.y - wd.x);
 }
-// C2R pre step for bin k from X_k, X_{SH-k} and W_S^k: E + i O with E = (X_k + X*_{SH-k})/2,
-// O = (X_k - X*_{SH-k})/2 conj(W^k)
+// C2R pre step for bin k from X_k, X_{SH-k} and W_S^k: 2 (E + i O) with 2 E = X_k + X*_{SH-k},
+// 2 O = (X_k - X*_{SH-k}) conj(W^k)
 __device__ __forceinline__ float2 c2r_pre(float2 xk, float2 xp, float2 w) {
-    const float2 e = make_float2(0.5f * (xk.x + xp.x), 0.5f * (xk.y - xp.y));
-    const float2 d = make_float2(0.5f * (xk.x - xp.x), 0.5f * (xk.y + xp.y));
+    const float2 e = make_float2(xk.x + xp.x, xk.y - xp.y);
+    const float2 d = make_float2(xk.x - xp.x, xk.y + xp.y);
     const float2 o = cmul(d, conjf2(w));
     return make_float2(e.x - o.y, e.y + o.x);
 }
@@ -493,18 +497,22 @@ __global__ void __launch_bounds__(256) k_rows_fwd(FftArgs A, int mode, int par, 
         __syncthreads();
         // R2C post-processing, one (k, SH - k) pair per item (both outputs read the same two
         // values; W^{SH-k} = -conj W^k); the self-paired k = SH/2 is done by the k = 0 item
-        constexpr int HP = SH / 2;
-        for (int idx = tid; idx < NB * HP; idx += G::NTH) {
-            const int rr = idx / HP, k = idx % HP;
+        // thread -> fixed k, rows rr0, rr0 + RPP, ... (twiddles and row pointer set once)
+        constexpr int HP = SH / 2, RPP = G::NTH / HP;
+        static_assert(G::NTH % HP == 0 && NB % RPP == 0, "post-processing split");
+        const int k = tid % HP, rr0 = tid / HP;
+        const float2 w = Wsm[k], wc = make_float2(-w.x, w.y), wm = Wsm[HP];
+        float2 *dst = (mode == 2) ? hrows + ((int64_t)tile * S + r0 + rr0) * LDF
+                                  : A.scratch + (int64_t)tile * A.tile_rows * LDF + ((int64_t)qi * S + r0 + rr0) * LDF;
+#pragma unroll 4
+        for (int rr = rr0; rr < NB; rr += RPP, dst += RPP * LDF) {
             const float2 *wr = work + rr * RS;
-            float2 *dst = (mode == 2) ? hrows + ((int64_t)tile * S + r0 + rr) * LDF
-                                      : A.scratch + (int64_t)tile * A.tile_rows * LDF + ((int64_t)qi * S + r0 + rr) * LDF;
-            const float2 a = wr[k], b = wr[(SH - k) & (SH - 1)], w = Wsm[k];
+            const float2 a = wr[k], b = wr[(SH - k) & (SH - 1)];
             dst[k] = r2c_post(a, b, w);
-            dst[SH - k] = r2c_post(b, a, make_float2(-w.x, w.y));
+            dst[SH - k] = r2c_post(b, a, wc);
             if (k == 0) {
                 const float2 m = wr[HP];
-                dst[HP] = r2c_post(m, m, Wsm[HP]);
+                dst[HP] = r2c_post(m, m, wm);
             }
         }
     }
@@ -1173,18 +1181,21 @@ struct C2R {
     // half-length complex input z = E + i O from the staged spectrum rows -> work, one
     // (k, SH - k) pair per item; the self-paired k = SH/2 is done by the k = 0 item
     __device__ static __forceinline__ void pre(float2 *work, const float2 *stg, const float2 *Wsm, int tid) {
-        constexpr int HP = SH / 2;
-        for (int idx = tid; idx < NB * HP; idx += G::NTH) {
-            const int rr = idx / HP, k = idx % HP;
+        constexpr int HP = SH / 2, RPP = G::NTH / HP;
+        static_assert(G::NTH % HP == 0 && NB % RPP == 0, "pre-processing split");
+        const int k = tid % HP, rr0 = tid / HP;
+        const float2 w = Wsm[k], wc = make_float2(-w.x, w.y), wm = Wsm[HP];
+#pragma unroll 4
+        for (int rr = rr0; rr < NB; rr += RPP) {
             const float2 *sr = stg + rr * SS;
             float2 *wr = work + rr * RS;
-            const float2 a = sr[k], b = sr[SH - k], w = Wsm[k];
+            const float2 a = sr[k], b = sr[SH - k];
             wr[k] = c2r_pre(a, b, w);
             if (k == 0) {
                 const float2 m = sr[HP];
-                wr[HP] = c2r_pre(m, m, Wsm[HP]);
+                wr[HP] = c2r_pre(m, m, wm);
             } else {
-                wr[SH - k] = c2r_pre(b, a, make_float2(-w.x, w.y));
+                wr[SH - k] = c2r_pre(b, a, wc);
             }
         }
     }
@@ -1420,7 +1431,7 @@ struct FftPlan {
         a.wy = wy; a.wx = wx; a.Ny = Ny; a.Nx = Nx; a.P = P; a.Gx = Gx;
         a.scratch = scratch; a.tile_rows = tile_rows; a.NQ = NQ; a.NP = NP;
         a.partials = partials;
-        a.scale = 2.0f / ((float)S * (float)S);
+        a.scale = 0.25f / ((float)S * (float)S);   // 2 / S^2 (C2R) / 8 (the omitted 1/2 factors, r2c_post / c2r_pre)
         return a;
     }
 };

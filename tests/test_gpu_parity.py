@@ -118,11 +118,41 @@ def test_gpu_identical_and_delta_psfs():
         assert rel_l2(dev.apply_H(x), x[c:n - c, c:n - c]) <= 1e-6
 
 
+def dense_blocks(centres, lim_y, lim_x, half=24):
+    """All pixels of the (2 half)^2 blocks around `centres`, clipped to the image."""
+    ii, jj = [], []
+    for cy, cx in centres:
+        y0, x0 = min(max(cy - half, 0), lim_y - 2 * half), min(max(cx - half, 0), lim_x - 2 * half)
+        yy, xx = np.meshgrid(np.arange(y0, y0 + 2 * half), np.arange(x0, x0 + 2 * half), indexing="ij")
+        ii.append(yy.ravel())
+        jj.append(xx.ravel())
+    return np.concatenate(ii), np.concatenate(jj)
+
+
+def structural_centres(pb, observed):
+    """Image corners, facet-seam crossings (A12 bounds) and, in facet 0, the first FFT
+    tile boundary (T = 512 - P + 1) and the start of the last, ragged tile row/column."""
+    from oracle import geometry
+    fac = geometry.plan(pb.ny, pb.nx, pb.P, pb.fy, pb.fx, pb.overlap)
+    ly, lx = (pb.my, pb.mx) if observed else (pb.ny, pb.nx)
+    T = 512 - pb.P + 1
+    f0 = fac[0]
+    (y0, y1), (x0, x1) = (f0.oy, f0.ox) if observed else (f0.ey, f0.ex)
+    c = [(0, 0), (ly - 1, lx - 1), (0, lx - 1), (ly - 1, 0),
+         (y0 + T, x0 + T), (y0 + ((y1 - y0) // T) * T, x0 + ((x1 - x0) // T) * T)]
+    for f in fac[1:]:
+        (a0, _), (b0, _) = (f.oy, f.ox) if observed else (f.ey, f.ex)
+        c.append((a0 + (pb.overlap + pb.P) // 2, b0 + (pb.overlap + pb.P) // 2))   # inside the shared band
+    return c
+
+
 @pytest.mark.parametrize("path", PATHS, ids=["direct", "fft"])
-@pytest.mark.parametrize("k,count", [(3, 4000), (4, 3000)])
+@pytest.mark.parametrize("k,count", [(3, 20000), (4, 100000)])
 def test_apply_full_size_sampled(k, count, path):
     """BASELINE full sizes (c3 4096^2, c4 16384^2), bench launch configuration,
-    checked on sampled pixels the oracle evaluates one by one."""
+    checked on pixels the oracle evaluates one by one (1e5 random pixels at
+    c4) plus dense 48x48 blocks across the structural boundaries: image corners, facet
+    seams and shared bands, FFT tile and ragged-strip boundaries."""
     pb = synth.make_config(k)
     rng = np.random.default_rng(k)
     x = (0.05 + rng.random((pb.ny, pb.nx), dtype=np.float32) * 0.5).astype(np.float32)
@@ -131,15 +161,18 @@ def test_apply_full_size_sampled(k, count, path):
     with D.Deblur.from_problem(pb, conv_path=path) as dev:
         hx = dev.apply_H(x)
         g = dev.apply_HT(r)
-    oi, oj = rng.integers(0, pb.my, count), rng.integers(0, pb.mx, count)
-    # include facet seams and image borders
-    oi[:8] = [0, pb.my - 1, 0, pb.my - 1, pb.my // 2, pb.my // 4, 1, pb.my - 2]
+    bi, bj = dense_blocks(structural_centres(pb, True), pb.my, pb.mx)
+    oi = np.concatenate([rng.integers(0, pb.my, count), bi])
+    oj = np.concatenate([rng.integers(0, pb.mx, count), bj])
     ref = op.H_points(x, oi, oj)
     assert rel_l2(hx[oi, oj], ref) <= H_TOL
-    ei, ej = rng.integers(0, pb.ny, count), rng.integers(0, pb.nx, count)
-    ei[:4] = [0, pb.ny - 1, 31, pb.ny - 32]
+    assert rel_l2(hx[bi, bj], ref[count:]) <= H_TOL
+    bi, bj = dense_blocks(structural_centres(pb, False), pb.ny, pb.nx)
+    ei = np.concatenate([rng.integers(0, pb.ny, count), bi])
+    ej = np.concatenate([rng.integers(0, pb.nx, count), bj])
     ref = op.HT_points(r, ei, ej)
     assert rel_l2(g[ei, ej], ref) <= H_TOL
+    assert rel_l2(g[bi, bj], ref[count:]) <= H_TOL
 
 
 # ------------------------------------------------------------------ iterate
