@@ -51,6 +51,9 @@
 #ifndef COLS_TM_TWTMEM
 #define COLS_TM_TWTMEM 1   // per-thread twiddles of the TMEM column pass in TMEM
 #endif
+#ifndef COLS_TM_CPB
+#define COLS_TM_CPB 3      // column chunks per CTA of the TMEM column pass (257 columns = 33 chunks of 8)
+#endif
 #ifndef COLS_TM_MINB
 #define COLS_TM_MINB (16 / COLS_TM_NB)
 #endif
@@ -904,8 +907,10 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
     int *slot_s = reinterpret_cast<int *>(wys_all + (size_t)A.NP * S);
     uint32_t *tm_slot = reinterpret_cast<uint32_t *>(slot_s + A.NP * A.NQ);
     const int tid = threadIdx.x, warp = tid >> 5;
-    const int nchunk = (NF + NB - 1) / NB;
-    const int tile = blockIdx.x / nchunk, f0 = (blockIdx.x % nchunk) * NB;
+    // COLS_TM_CPB consecutive column chunks of one tile per CTA: the TMEM allocation,
+    // twiddles and the tile's wy_p rows / PSF slots are set up once for all of them
+    const int nchunk = (NF + NB - 1) / NB, ngrp = (nchunk + COLS_TM_CPB - 1) / COLS_TM_CPB;
+    const int tile = blockIdx.x / ngrp, cg = blockIdx.x % ngrp;
     const int P = A.P, c2 = P - 1, T = S - P + 1;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
@@ -962,6 +967,9 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
     const TwTable tw{Wsm, S};
 #endif
     const int nqt = td.q1 - td.q0 + 1;
+    for (int ci = 0; ci < COLS_TM_CPB; ++ci) {
+    const int f0 = (cg * COLS_TM_CPB + ci) * NB;
+    if (f0 >= NF) break;
     auto hk = [&](int p, int q) { return A.Hhat + (int64_t)slot_s[(p - td.p0) * nqt + (q - td.q0)] * S * LDF; };
     // stage-0 input positions of this thread, straight from the global chunk (row stride LDF)
     auto load_in = [&](const float2 *src, float2 (&v)[E]) {
@@ -1142,6 +1150,8 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
                 }
             }
         }
+    }
+    __syncthreads();                               // smem buffers free for the next chunk
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
@@ -1521,7 +1531,7 @@ static cudaError_t run_cols(const FftArgs &a, int ntiles, int mode, const float2
 #if COLS_TMEM
     if constexpr (S == 512) {
         if (mode != 2) {
-            k_cols_tm<S><<<ntiles * nchunk, GCT<S>::NTH, smem_cols_tm<S>(a.NP, a.NQ), s>>>(a, mode);
+            k_cols_tm<S><<<ntiles * ((nchunk + COLS_TM_CPB - 1) / COLS_TM_CPB), GCT<S>::NTH, smem_cols_tm<S>(a.NP, a.NQ), s>>>(a, mode);
             return cudaGetLastError();
         }
     }
