@@ -54,6 +54,9 @@
 #ifndef COLS_TM_CPB
 #define COLS_TM_CPB 3      // column chunks per CTA of the TMEM column pass (257 columns = 33 chunks of 8)
 #endif
+#ifndef COLS_TM_NYQ
+#define COLS_TM_NYQ 1      // TMEM column pass: Nyquist column packed into column 0 (32 chunks, not 33)
+#endif
 #ifndef COLS_TM_MINB
 #define COLS_TM_MINB (16 / COLS_TM_NB)
 #endif
@@ -546,6 +549,13 @@ __device__ __forceinline__ void prefetch_hhat(float2 *hbuf, const float2 *Hk, in
     }
     __pipeline_commit();
 }
+// column S/2 (Nyquist) of a pair-interleaved PSF spectrum -> hn[0, S) (not committed: the
+// prefetch_hhat that follows commits it with the chunk)
+template <int S, int NTH, int LDF>
+__device__ __forceinline__ void prefetch_hnyq(float2 *hn, const float2 *Hk, int tid) {
+    for (int m = tid; m < S / 2; m += NTH)
+        __pipeline_memcpy_async(hn + 2 * m, Hk + (((int64_t)m * LDF + S / 2) << 1), 16);
+}
 __device__ __forceinline__ float4 ld4(const float2 *p) { return *reinterpret_cast<const float4 *>(p); }
 __device__ __forceinline__ float2 lo2(float4 q) { return make_float2(q.x, q.y); }
 __device__ __forceinline__ float2 hi2(float4 q) { return make_float2(q.z, q.w); }
@@ -886,8 +896,11 @@ struct GCT {
 template <int S>
 static size_t smem_cols_tm(int NP, int NQ) {
     using G = GCT<S>;
-    return (size_t)COLS_TM_TW * 8 + (size_t)S * G::NB * 8 + (size_t)G::NB * G::CS * 8 + (size_t)NP * S * 4 +
-           (size_t)NP * NQ * 4 + 16;
+#ifndef COLS_TM_SMEM_PAD
+#define COLS_TM_SMEM_PAD 0
+#endif
+    return (size_t)COLS_TM_TW * 8 + (size_t)S * G::NB * 8 + (size_t)G::NB * G::CS * 8 + (COLS_TM_NYQ ? 2 * (size_t)S * 8 : 0) +
+           (size_t)NP * S * 4 + (size_t)NP * NQ * 4 + 16 + COLS_TM_SMEM_PAD;
 }
 
 template <int S>
@@ -903,13 +916,21 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
     float2 *Wsm = sm2;               // S
     float2 *hbuf = Wsm + COLS_TM_TW; // S x NB (prefetched PSF spectrum chunk, pair-interleaved)
     float2 *work = hbuf + S * NB;    // NB x CS
-    float *wys_all = reinterpret_cast<float *>(work + NB * CS);
+    float2 *hnq = work + NB * CS;    // S: Nyquist column of the PSF spectrum (chunk 0)
+    float2 *nyq = hnq + (COLS_TM_NYQ ? S : 0);   // S: the packed column's spectrum C (chunk 0)
+    float *wys_all = reinterpret_cast<float *>(nyq + (COLS_TM_NYQ ? S : 0));
     int *slot_s = reinterpret_cast<int *>(wys_all + (size_t)A.NP * S);
     uint32_t *tm_slot = reinterpret_cast<uint32_t *>(slot_s + A.NP * A.NQ);
     const int tid = threadIdx.x, warp = tid >> 5;
     // COLS_TM_CPB consecutive column chunks of one tile per CTA: the TMEM allocation,
     // twiddles and the tile's wy_p rows / PSF slots are set up once for all of them
-    const int nchunk = (NF + NB - 1) / NB, ngrp = (nchunk + COLS_TM_CPB - 1) / COLS_TM_CPB;
+    // with COLS_TM_NYQ the real columns 0 (DC) and S/2 (Nyquist) of the row spectra travel
+    // as one complex column c = X[., 0] + i X[., S/2] in chunk 0's column 0: S/2 columns
+    static_assert(!COLS_TM_NYQ || (S / 2) % NB == 0, "Nyquist packing needs whole chunks");
+    // (H only: for H^T the per-(p, q) combination of the packed column measured slower)
+    const bool nyq_on = COLS_TM_NYQ && mode == 0;
+    const int nchunk = nyq_on ? (S / 2) / NB : (NF + NB - 1) / NB;
+    const int ngrp = (nchunk + COLS_TM_CPB - 1) / COLS_TM_CPB;
     const int tile = blockIdx.x / ngrp, cg = blockIdx.x % ngrp;
     const int P = A.P, c2 = P - 1, T = S - P + 1;
     if (warp == 0) {
@@ -969,7 +990,12 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
     const int nqt = td.q1 - td.q0 + 1;
     for (int ci = 0; ci < COLS_TM_CPB; ++ci) {
     const int f0 = (cg * COLS_TM_CPB + ci) * NB;
-    if (f0 >= NF) break;
+    if (f0 >= nchunk * NB) break;
+    // this thread carries the packed (DC, Nyquist) column: its spectrum C_n = A_n + i B_n
+    // (A, B the DFTs of the two real columns, Hermitian) is multiplied as
+    // M0 A + i MN B = ((M0 + MN) C_n + (M0 - MN) conj C_{-n}) / 2 (M = the PSF spectrum's
+    // columns 0 and S/2); the inverse DFT of that is real_0 + i real_N
+    const bool pk = nyq_on && f0 == 0 && (tid % NB) == 0;
     auto hk = [&](int p, int q) { return A.Hhat + (int64_t)slot_s[(p - td.p0) * nqt + (q - td.q0)] * S * LDF; };
     // stage-0 input positions of this thread, straight from the global chunk (row stride LDF)
     auto load_in = [&](const float2 *src, float2 (&v)[E]) {
@@ -978,8 +1004,19 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
             int t, j;
             S0::bj(i, tid, t, j);
 #pragma unroll
-            for (int r = 0; r < S0::R; ++r) v[i * S0::R + r] = __ldg(src + (int64_t)S0::in_n(j, r) * LDF + f0 + t);
+            for (int r = 0; r < S0::R; ++r) {
+                const float2 *sp = src + (int64_t)S0::in_n(j, r) * LDF + f0 + t;
+                v[i * S0::R + r] = __ldg(sp);
+                if (pk) v[i * S0::R + r].y = __ldg(sp + S / 2).x;   // X[., 0] and X[., S/2] are real
+            }
         }
+    };
+    // packed column: store / combine through nyq (positions n of this thread's elements)
+    auto nyq_mul = [&](float2 c, int n, float2 m0, float2 mn) {
+        const float2 cm = conjf2(nyq[(S - n) & (S - 1)]);
+        const float2 a = cadd(m0, mn), b = csub(m0, mn);
+        const float2 r = cadd(cmul(a, c), cmul(b, cm));
+        return make_float2(0.5f * r.x, 0.5f * r.y);
     };
     float2 v[E];
 
@@ -991,6 +1028,7 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
             tm_wait_st();
             for (int p = td.p0; p <= td.p1; ++p) {
                 __syncthreads();                   // hbuf free
+                if (nyq_on && f0 == 0) prefetch_hnyq<S, NTH, LDF>(hnq, hk(p, q), tid);
                 prefetch_hhat<S, NB, NTH, LDF>(hbuf, hk(p, q), f0, tid);   // under the FFT below
                 const float *wys = wys_all + (size_t)(p - td.p0) * S;
                 if (p != td.p0) tm_get<E>(t_in, v);
@@ -1009,8 +1047,31 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
                     S0::template bfly<-1>(&v[(i + 1) * S0::R], j + 1, Wsm, S);
                 }
                 F::template middle_tw<-1>(work, v, tid, tw);
+                if (pk) {
+#pragma unroll
+                    for (int i = 0; i < SL::BPT; ++i) {
+                        int t, j;
+                        SL::bj(i, tid, t, j);
+#pragma unroll
+                        for (int r = 0; r < SL::R; ++r) nyq[SL::out_n(j, r)] = v[i * SL::R + r];
+                    }
+                }
                 __pipeline_wait_prior(0);
-                __syncthreads();                   // Hhat chunk visible
+                __syncthreads();                   // Hhat chunk (and nyq) visible
+                if (pk) {
+#pragma unroll
+                    for (int i = 0; i < SL::BPT; ++i) {
+                        int t, j;
+                        SL::bj(i, tid, t, j);
+#pragma unroll
+                        for (int r = 0; r < SL::R; ++r) {
+                            const int n = SL::out_n(j, r);
+                            float2 &h0 = hbuf[hb_idx<NB>(n, 0)];   // read only by this thread
+                            v[i * SL::R + r] = nyq_mul(v[i * SL::R + r], n, h0, hnq[n]);
+                            h0 = make_float2(1.f, 0.f);           // the product below is then v itself
+                        }
+                    }
+                }
                 // acc += v . Hhat, in two halves of 8 complex (16 TMEM columns each)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
@@ -1063,7 +1124,14 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
 #pragma unroll
             for (int r = 0; r < SL::R; ++r) {
                 const int n = SL::out_n(j, r);
-                if (n >= c2) O[(int64_t)(n - c2) * LDF + t] = v[i * SL::R + r];
+                if (n >= c2) {
+                    if (pk) {
+                        O[(int64_t)(n - c2) * LDF] = make_float2(v[i * SL::R + r].x, 0.f);
+                        O[(int64_t)(n - c2) * LDF + S / 2] = make_float2(v[i * SL::R + r].y, 0.f);
+                    } else {
+                        O[(int64_t)(n - c2) * LDF + t] = v[i * SL::R + r];
+                    }
+                }
             }
         }
     } else {
@@ -1531,7 +1599,8 @@ static cudaError_t run_cols(const FftArgs &a, int ntiles, int mode, const float2
 #if COLS_TMEM
     if constexpr (S == 512) {
         if (mode != 2) {
-            k_cols_tm<S><<<ntiles * ((nchunk + COLS_TM_CPB - 1) / COLS_TM_CPB), GCT<S>::NTH, smem_cols_tm<S>(a.NP, a.NQ), s>>>(a, mode);
+            const int nck = (COLS_TM_NYQ && mode == 0) ? (S / 2) / GCT<S>::NB : nchunk;
+            k_cols_tm<S><<<ntiles * ((nck + COLS_TM_CPB - 1) / COLS_TM_CPB), GCT<S>::NTH, smem_cols_tm<S>(a.NP, a.NQ), s>>>(a, mode);
             return cudaGetLastError();
         }
     }
