@@ -52,7 +52,7 @@
 #define COLS_TM_TWTMEM 1   // per-thread twiddles of the TMEM column pass in TMEM
 #endif
 #ifndef COLS_TM_CPB
-#define COLS_TM_CPB 3      // column chunks per CTA of the TMEM column pass (257 columns = 33 chunks of 8)
+#define COLS_TM_CPB 3      // column chunks per CTA of the TMEM column pass (when the grid stays >= 4 waves)
 #endif
 #ifndef COLS_TM_NYQ
 #define COLS_TM_NYQ 1      // TMEM column pass: Nyquist column packed into column 0 (32 chunks, not 33)
@@ -904,7 +904,7 @@ static size_t smem_cols_tm(int NP, int NQ) {
 }
 
 template <int S>
-__global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftArgs A, int mode) {
+__global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftArgs A, int mode, int cpb) {
     using G = GCT<S>;
     using F = typename G::F;
     using S0 = typename F::First;
@@ -922,7 +922,7 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
     int *slot_s = reinterpret_cast<int *>(wys_all + (size_t)A.NP * S);
     uint32_t *tm_slot = reinterpret_cast<uint32_t *>(slot_s + A.NP * A.NQ);
     const int tid = threadIdx.x, warp = tid >> 5;
-    // COLS_TM_CPB consecutive column chunks of one tile per CTA: the TMEM allocation,
+    // cpb consecutive column chunks of one tile per CTA: the TMEM allocation,
     // twiddles and the tile's wy_p rows / PSF slots are set up once for all of them
     // with COLS_TM_NYQ the real columns 0 (DC) and S/2 (Nyquist) of the row spectra travel
     // as one complex column c = X[., 0] + i X[., S/2] in chunk 0's column 0: S/2 columns
@@ -930,7 +930,7 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
     // (H only: for H^T the per-(p, q) combination of the packed column measured slower)
     const bool nyq_on = COLS_TM_NYQ && mode == 0;
     const int nchunk = nyq_on ? (S / 2) / NB : (NF + NB - 1) / NB;
-    const int ngrp = (nchunk + COLS_TM_CPB - 1) / COLS_TM_CPB;
+    const int ngrp = (nchunk + cpb - 1) / cpb;
     const int tile = blockIdx.x / ngrp, cg = blockIdx.x % ngrp;
     const int P = A.P, c2 = P - 1, T = S - P + 1;
     if (warp == 0) {
@@ -988,8 +988,8 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
     const TwTable tw{Wsm, S};
 #endif
     const int nqt = td.q1 - td.q0 + 1;
-    for (int ci = 0; ci < COLS_TM_CPB; ++ci) {
-    const int f0 = (cg * COLS_TM_CPB + ci) * NB;
+    for (int ci = 0; ci < cpb; ++ci) {
+    const int f0 = (cg * cpb + ci) * NB;
     if (f0 >= nchunk * NB) break;
     // this thread carries the packed (DC, Nyquist) column: its spectrum C_n = A_n + i B_n
     // (A, B the DFTs of the two real columns, Hermitian) is multiplied as
@@ -1600,7 +1600,16 @@ static cudaError_t run_cols(const FftArgs &a, int ntiles, int mode, const float2
     if constexpr (S == 512) {
         if (mode != 2) {
             const int nck = (COLS_TM_NYQ && mode == 0) ? (S / 2) / GCT<S>::NB : nchunk;
-            k_cols_tm<S><<<ntiles * ((nck + COLS_TM_CPB - 1) / COLS_TM_CPB), GCT<S>::NTH, smem_cols_tm<S>(a.NP, a.NQ), s>>>(a, mode);
+            // several chunks per CTA only while the grid keeps >= 4 waves of 2 CTAs per SM
+            static int nsm = 0;
+            if (!nsm) {
+                int dev = 0;
+                cudaGetDevice(&dev);
+                if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm <= 0) nsm = 148;
+            }
+            int cpb = COLS_TM_CPB;
+            while (cpb > 1 && (int64_t)ntiles * ((nck + cpb - 1) / cpb) < 8LL * nsm) --cpb;
+            k_cols_tm<S><<<ntiles * ((nck + cpb - 1) / cpb), GCT<S>::NTH, smem_cols_tm<S>(a.NP, a.NQ), s>>>(a, mode, cpb);
             return cudaGetLastError();
         }
     }
