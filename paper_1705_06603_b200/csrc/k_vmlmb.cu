@@ -250,6 +250,7 @@ __global__ void __launch_bounds__(VNT) k_grad(VmArgs a, SolverConst sc) {
     constexpr int XH = VT_X + 8;
     __shared__ __align__(16) float xh[(VT_Y + 2) * XH];
     __shared__ double red[3 * 8];
+    __shared__ float om_c[VT_X], om_r[VT_Y];
     const TileDesc t = a.tiles[blockIdx.x];
     const FacetDev &F = a.facets[t.f];
     const float *__restrict__ x = F.x[a.par];
@@ -280,24 +281,50 @@ __global__ void __launch_bounds__(VNT) k_grad(VmArgs a, SolverConst sc) {
             xh[idx] = x[(int64_t)fy * F.ep + fx];
         }
     }
+    // omega^F once per tile column / row (A13 ramps are 1 off the bands, so the product is the
+    // pixel's weight everywhere; per-node weight rows likewise)
+    if (threadIdx.x < VT_X) {
+        const int fx = t.x0 + threadIdx.x;
+        om_c[threadIdx.x] = fx < F.nx ? omega_axis(F.ax, fx) : 1.f;
+    } else if (threadIdx.x < VT_X + VT_Y) {
+        const int fy = t.y0 + threadIdx.x - VT_X;
+        om_r[threadIdx.x - VT_X] = fy < F.ny ? omega_axis(F.ay, fy) : 1.f;
+    }
     __syncthreads();
-    float *G = a.A[t.f];
+    // facet fields in registers: the G stores could alias them for the compiler
+    float *__restrict__ G = a.A[t.f];
+    const float *__restrict__ up = F.u;
+    const float *__restrict__ gp = F.g;
+    const int ny = F.ny, nx = F.nx;
+    const int64_t ep = F.ep;
     double reg = 0.0, prox = 0.0;
-    for_tile4(F, t, [&](int64_t o4, int fy, int fx4, int nv) {
-      for (int jj = 0; jj < nv; ++jj) {
-        const int fx = fx4 + jj;
-        const int64_t o = o4 + jj;
-        const int ly = fy - t.y0, lx = fx - t.x0;
-        float phi;
-        const float tdiv = tv_grad_t<REG, NEU>(F.ny, F.nx, xh, XH, ly + 1, lx + 4, fy, fx, sc, true, phi);
-        const float xc = xh[(ly + 1) * XH + lx + 4], uc = F.u[o];
-        const bool shared = fy < F.ay.b_prev || fy >= F.ay.b_next || fx < F.ax.b_prev || fx >= F.ax.b_next;
-        const float om = (shared || F.ay.w) ? omega_axis(F.ay, fy) * omega_axis(F.ax, fx) : 1.f;
-        G[o] = F.g[o] + sc.lambda * tdiv + sc.gamma * om * (xc - uc);
-        reg += (double)phi;
-        prox += 0.5 * (double)sc.gamma * (double)om * ((double)xc - uc) * ((double)xc - uc);
-      }
-    });
+#pragma unroll
+    for (int i = 0; i < VT_Y * VT_X / 4 / VNT; ++i) {
+        const int gi = threadIdx.x + VNT * i;
+        const int ly = gi >> 5, lx4 = 4 * (gi & 31);
+        const int fy = t.y0 + ly, fx4 = t.x0 + lx4;
+        if (fy >= ny || fx4 >= nx) continue;
+        const int nv = min(4, nx - fx4);
+        const int64_t o4 = (int64_t)fy * ep + fx4;
+        float uv[4], gv[4], out[4];
+        ld4(up + o4, nv, uv);
+        ld4(gp + o4, nv, gv);
+        const float omy = om_r[ly];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+            const int fx = fx4 + jj;
+            float phi;
+            const float tdiv = tv_grad_t<REG, NEU>(ny, nx, xh, XH, ly + 1, lx4 + jj + 4, fy, fx, sc, true, phi);
+            const float xc = xh[(ly + 1) * XH + lx4 + jj + 4], uc = uv[jj];
+            const float om = omy * om_c[lx4 + jj];
+            out[jj] = gv[jj] + sc.lambda * tdiv + sc.gamma * om * (xc - uc);
+            if (jj < nv) {
+                reg += (double)phi;
+                prox += 0.5 * (double)sc.gamma * (double)om * ((double)xc - uc) * ((double)xc - uc);
+            }
+        }
+        st4(G + o4, nv, out);
+    }
     block_sum3(reg, red, 0);
     block_sum3(prox, red, 1);
     block_finish(red, 2, a.partials, a.ntiles);
