@@ -896,11 +896,8 @@ struct GCT {
 template <int S>
 static size_t smem_cols_tm(int NP, int NQ) {
     using G = GCT<S>;
-#ifndef COLS_TM_SMEM_PAD
-#define COLS_TM_SMEM_PAD 0
-#endif
     return (size_t)COLS_TM_TW * 8 + (size_t)S * G::NB * 8 + (size_t)G::NB * G::CS * 8 + (COLS_TM_NYQ ? 2 * (size_t)S * 8 : 0) +
-           (size_t)NP * S * 4 + (size_t)NP * NQ * 4 + 16 + COLS_TM_SMEM_PAD;
+           (size_t)NP * S * 4 + (size_t)NP * NQ * 4 + 16;
 }
 
 template <int S>
