@@ -1598,12 +1598,12 @@ static cudaError_t run_cols(const FftArgs &a, int ntiles, int mode, const float2
         if (mode != 2) {
             const int nck = (COLS_TM_NYQ && mode == 0) ? (S / 2) / GCT<S>::NB : nchunk;
             // several chunks per CTA only while the grid keeps >= 4 waves of 2 CTAs per SM
-            static int nsm = 0;
-            if (!nsm) {
-                int dev = 0;
+            static const int nsm = [] {       // thread-safe one-time init (one GPU per process)
+                int dev = 0, n = 0;
                 cudaGetDevice(&dev);
-                if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm <= 0) nsm = 148;
-            }
+                if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+                return n;
+            }();
             int cpb = COLS_TM_CPB;
             while (cpb > 1 && (int64_t)ntiles * ((nck + cpb - 1) / cpb) < 8LL * nsm) --cpb;
             k_cols_tm<S><<<ntiles * ((nck + cpb - 1) / cpb), GCT<S>::NTH, smem_cols_tm<S>(a.NP, a.NQ), s>>>(a, mode, cpb);
