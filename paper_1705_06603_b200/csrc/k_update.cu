@@ -191,7 +191,15 @@ __device__ __forceinline__ float view_at(const View &v, int par, int gy, int gx)
 // neighbour offsets are constant on the piece: their descriptors (v pointer at this
 // column, pitch, omega along x) are resolved once per thread and the rows' omega along
 // y once per CTA (shared memory), so the row loop is loads + arithmetic only.
-__global__ void __launch_bounds__(256) k_consensus(const FacetDev *facets, const BandRect *rects,
+// K5_GR rows per load batch, 4 CTAs/SM (61 registers): per-node c4, where almost every pixel
+// is shared by 4 facets, 7.2 -> 5.8 ms against 8 rows at 2 CTAs/SM (profiles/r1/SUMMARY.md)
+#ifndef K5_GR
+#define K5_GR 2            // rows whose loads are in flight together
+#endif
+#ifndef K5_MINB
+#define K5_MINB 4
+#endif
+__global__ void __launch_bounds__(256, K5_MINB) k_consensus(const FacetDev *facets, const BandRect *rects,
                                                    const RectTile *tiles, int par, float rho) {
     __shared__ float omy_s[2][CT_ROWS];
     const RectTile T = tiles[blockIdx.x];
@@ -227,12 +235,13 @@ __global__ void __launch_bounds__(256) k_consensus(const FacetDev *facets, const
     const int64_t ep = F.ep;
     float *__restrict__ up = F.u + (int64_t)T.y0 * ep + lx;
     const float *__restrict__ xp = F.x[par] + (int64_t)T.y0 * ep + lx;
-    for (int g = 0; g < nr; g += 8) {
-        // every load of 8 rows in flight before the first use (v / x through the
-        // read-only path: the u stores cannot alias them)
-        float vv[8][4], xv[8], uv[8];
+    for (int g = 0; g < nr; g += K5_GR) {
+        // every load of K5_GR rows in flight before the first use (v / x through the
+        // read-only path: the u stores cannot alias them); more rows hold more registers
+        // than 4 CTAs/SM allow
+        float vv[K5_GR][4], xv[K5_GR], uv[K5_GR];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
+        for (int r = 0; r < K5_GR; ++r) {
             const bool ok = g + r < nr;
             const int64_t rr = g + r;
 #pragma unroll
@@ -241,7 +250,7 @@ __global__ void __launch_bounds__(256) k_consensus(const FacetDev *facets, const
             uv[r] = ok ? up[rr * ep] : 0.f;
         }
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
+        for (int r = 0; r < K5_GR; ++r) {
             if (g + r >= nr) break;
             float num = 0.f, den = 0.f;
 #pragma unroll
