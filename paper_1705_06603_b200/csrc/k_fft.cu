@@ -1287,7 +1287,10 @@ __global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
     extern __shared__ __align__(16) float2 sm2[];
     float2 *Wsm = sm2;                                         // ROWS_TW(S) twiddles
     float2 *work = Wsm + ROWS_TW(S);                           // NB x RS; reused as outs (NB x XS reals)
-    float2 *stg = work + NB * RS;                              // NB x SS staging
+    // NB x SS staging; H has a single source, staged straight into work and pre-processed in
+    // place (C2R::pre reads and writes only its own (k, SH - k) pair): 3 -> 4 CTAs/SM
+    static_assert(C::SS == RS, "in-place staging");
+    float2 *stg = HT ? work + NB * RS : work;
     float *wxs = reinterpret_cast<float *>(stg + NB * C::SS);  // NQ x S (H^T)
     float *outs = reinterpret_cast<float *>(work);
     __shared__ double red[256 / 32];
@@ -1549,8 +1552,7 @@ static size_t smem_cols(int NP, int NQ) {
 template <int S>
 static size_t smem_rows_inv(int NQ, bool ht = true) {
     using G = GR<S>;
-    return (size_t)ROWS_TW(S) * 8 + (size_t)G::NB * G::RS * 8 + (size_t)G::NB * C2R<S>::SS * 8 +
-           (ht ? (size_t)NQ * S * 4 : 0);
+    return (size_t)ROWS_TW(S) * 8 + (size_t)G::NB * G::RS * 8 + (ht ? (size_t)G::NB * C2R<S>::SS * 8 + (size_t)NQ * S * 4 : 0);
 }
 
 // The dynamic-shared-memory limit is a property of the kernel function, shared by
