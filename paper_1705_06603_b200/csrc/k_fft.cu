@@ -370,7 +370,7 @@ struct LD {
 // ------------------------------------------------------------------ pass A / A'
 // mode 0: H (x window . wx_q, one R2C per active q); 1: H^T (r window); 2: PSF spectra rows
 template <int S>
-__global__ void __launch_bounds__(256) k_rows_fwd(FftArgs A, int mode, int par, const float *psfs, int npsf,
+__global__ void __launch_bounds__(256, S == 512 ? 4 : S == 1024 ? 2 : 5) k_rows_fwd(FftArgs A, int mode, int par, const float *psfs, int npsf,
                                                   float2 *hrows) {
     using G = GR<S>;
     using F = typename G::F;
@@ -378,7 +378,11 @@ __global__ void __launch_bounds__(256) k_rows_fwd(FftArgs A, int mode, int par, 
     extern __shared__ __align__(16) float2 sm2[];
     float2 *Wsm = sm2;                                      // ROWS_TW(S) twiddles
     float2 *work = Wsm + ROWS_TW(S);                        // NB x RS
-    float *xs = reinterpret_cast<float *>(work + NB * RS);  // NB x XS
+    // NB x XS real rows; at S = 512 with a single transform per CTA (modes 1, 2) they live in the
+    // exchange buffer (stage 0 reads them before the barrier that precedes the first exchange
+    // write): 4 CTAs/SM with <= 64 registers (H^T R2C 0.74 -> 0.62 ms)
+    static_assert(NB * XS <= 2 * NB * RS, "xs fits in work");
+    float *xs = reinterpret_cast<float *>((S == 512 && mode != 0) ? work : work + NB * RS);
     float *wxs = xs + NB * XS;                              // S
     const int tid = threadIdx.x;
     const int nblk = S / NB;
@@ -1540,9 +1544,10 @@ bool fft_prefer(int P) {
 }
 
 template <int S>
-static size_t smem_rows_fwd() {
+static size_t smem_rows_fwd(int mode = 0) {
     using G = GR<S>;
-    return (size_t)ROWS_TW(S) * 8 + (size_t)G::NB * G::RS * 8 + (size_t)G::NB * G::XS * 4 + (size_t)S * 4;
+    return (size_t)ROWS_TW(S) * 8 + (size_t)G::NB * G::RS * 8 +
+           ((S == 512 && mode != 0) ? 0 : (size_t)G::NB * G::XS * 4 + (size_t)S * 4);
 }
 template <int S>
 static size_t smem_cols(int NP, int NQ) {
@@ -1587,7 +1592,7 @@ template <int S>
 static cudaError_t run_rows_fwd(const FftArgs &a, int ntiles, int mode, int par, const float *psfs, int npsf,
                                 float2 *hrows, cudaStream_t s) {
     if (ntiles == 0) return cudaSuccess;
-    k_rows_fwd<S><<<ntiles * (S / GR<S>::NB), GR<S>::NTH, smem_rows_fwd<S>(), s>>>(a, mode, par, psfs, npsf, hrows);
+    k_rows_fwd<S><<<ntiles * (S / GR<S>::NB), GR<S>::NTH, smem_rows_fwd<S>(mode), s>>>(a, mode, par, psfs, npsf, hrows);
     return cudaGetLastError();
 }
 template <int S>
