@@ -54,6 +54,9 @@
 #ifndef COLS_TM_CPB
 #define COLS_TM_CPB 3      // column chunks per CTA of the TMEM column pass (when the grid stays >= 4 waves)
 #endif
+#ifndef ROWS_FWD_TMEM
+#define ROWS_FWD_TMEM 1    // R2C pass (H, S = 512): stage-0 inputs stashed in TMEM, xs aliases work
+#endif
 #ifndef COLS_TM_NYQ
 #define COLS_TM_NYQ 1      // TMEM column pass: Nyquist column packed into column 0 (32 chunks, not 33)
 #endif
@@ -367,9 +370,45 @@ struct LD {
     static constexpr int LDF = S / 2 + GC<S>::NB;   // padded spectrum row length (float2)
 };
 
+// tensor-memory helpers (32x32b shape: each thread its own lane, consecutive columns)
+__device__ __forceinline__ void tm_st32(uint32_t ta, const uint32_t (&r)[32]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%32], {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31};\n" :: "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]), "r"(ta) : "memory");
+}
+__device__ __forceinline__ void tm_ld32(uint32_t ta, uint32_t (&r)[32]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]) : "r"(ta) : "memory");
+}
+__device__ __forceinline__ void tm_st16(uint32_t ta, const uint32_t (&r)[16]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%16], {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15};\n" :: "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(ta) : "memory");
+}
+__device__ __forceinline__ void tm_ld16(uint32_t ta, uint32_t (&r)[16]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];\n" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]) : "r"(ta) : "memory");
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
+// E = 16 complex per thread <-> 32 TMEM columns
+template <int E>
+__device__ __forceinline__ void tm_put(uint32_t ta, const float2 (&v)[E]) {
+    static_assert(E == 16, "TMEM column pass holds 16 complex per thread");
+    uint32_t r[32];
+#pragma unroll
+    for (int e = 0; e < E; ++e) { r[2 * e] = __float_as_uint(v[e].x); r[2 * e + 1] = __float_as_uint(v[e].y); }
+    tm_st32(ta, r);
+}
+template <int E>
+__device__ __forceinline__ void tm_get(uint32_t ta, float2 (&v)[E]) {
+    uint32_t r[32];
+    tm_ld32(ta, r);
+    tm_wait_ld();
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = make_float2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
+}
+
 // ------------------------------------------------------------------ pass A / A'
 // mode 0: H (x window . wx_q, one R2C per active q); 1: H^T (r window); 2: PSF spectra rows
-template <int S>
+// TMX: the mode-0 instantiation with the TMEM stash (a kernel containing tcgen05 code ran
+// the other modes 2x slower, so they use the TMX = false instantiation)
+template <int S, bool TMX>
 __global__ void __launch_bounds__(256, S == 512 ? 4 : S == 1024 ? 2 : 5) k_rows_fwd(FftArgs A, int mode, int par, const float *psfs, int npsf,
                                                   float2 *hrows) {
     using G = GR<S>;
@@ -382,8 +421,13 @@ __global__ void __launch_bounds__(256, S == 512 ? 4 : S == 1024 ? 2 : 5) k_rows_
     // exchange buffer (stage 0 reads them before the barrier that precedes the first exchange
     // write): 4 CTAs/SM with <= 64 registers (H^T R2C 0.74 -> 0.62 ms)
     static_assert(NB * XS <= 2 * NB * RS, "xs fits in work");
-    float *xs = reinterpret_cast<float *>((S == 512 && mode != 0) ? work : work + NB * RS);
-    float *wxs = xs + NB * XS;                              // S
+    // Mode 0 (one transform per active q) at S = 512: each thread's stage-0 inputs are
+    // stashed in TMEM (32 columns) once, so xs can alias work there too (37 KB smem)
+    constexpr bool TMX_S = TMX;
+    const bool tmx = TMX;                 // launched for mode 0 only
+    float *xs = reinterpret_cast<float *>((S == 512 && (mode != 0 || tmx)) ? work : work + NB * RS);
+    float *wxs = tmx ? reinterpret_cast<float *>(work + NB * RS) : xs + NB * XS;   // S
+    __shared__ uint32_t tm_slot_x;
     const int tid = threadIdx.x;
     const int nblk = S / NB;
     const int tile = blockIdx.x / nblk, r0 = (blockIdx.x % nblk) * NB;
@@ -397,6 +441,11 @@ __global__ void __launch_bounds__(256, S == 512 ? 4 : S == 1024 ? 2 : 5) k_rows_
         t = A.tiles[tile];
         Fd = &A.facets[t.f];
         if (mode == 0) { q0 = t.q0; nq = t.q1 - t.q0 + 1; }
+    }
+    if (tmx && (tid >> 5) == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
+                     :: "r"((uint32_t)__cvta_generic_to_shared(&tm_slot_x)), "n"(64) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
     }
     for (int i = tid; i < ROWS_TW(S); i += G::NTH) Wsm[i] = A.W[i];
     {
@@ -460,6 +509,29 @@ __global__ void __launch_bounds__(256, S == 512 ? 4 : S == 1024 ? 2 : 5) k_rows_
             }
         }
     }
+    using S0 = typename F::First;
+    uint32_t t_x = 0;
+    if constexpr (TMX_S) {
+        if (tmx) {
+            static_assert(G::E == 16, "32 TMEM columns per thread");
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+            __syncthreads();                      // xs and the TMEM address visible
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            const int warp = tid >> 5;
+            t_x = tm_slot_x + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 32);
+            float2 z[G::E];
+#pragma unroll
+            for (int i = 0; i < S0::BPT; ++i) {
+                int tt, j;
+                S0::bj(i, tid, tt, j);
+#pragma unroll
+                for (int r = 0; r < S0::R; ++r) z[i * S0::R + r] = *reinterpret_cast<const float2 *>(xs + tt * XS + 2 * S0::in_n(j, r));
+            }
+            tm_put<G::E>(t_x, z);
+            tm_wait_st();
+            __syncthreads();                      // xs (= work) readers done
+        }
+    }
     // wx_q of the next active q in flight during this q's transform (mode 0)
     constexpr int WPT = (S + G::NTH - 1) / G::NTH;
     float wpre[WPT];
@@ -483,7 +555,9 @@ __global__ void __launch_bounds__(256, S == 512 ? 4 : S == 1024 ? 2 : 5) k_rows_
         __syncthreads();
         // stage 0 straight from the real rows: z[n] = (x[2n] w[2n], x[2n+1] w[2n+1])
         float2 v[G::E];
-        using S0 = typename F::First;
+        if constexpr (TMX_S) {
+            if (tmx) tm_get<G::E>(t_x, v);
+        }
 #pragma unroll
         for (int i = 0; i < S0::BPT; ++i) {
             int tt, j;
@@ -491,7 +565,7 @@ __global__ void __launch_bounds__(256, S == 512 ? 4 : S == 1024 ? 2 : 5) k_rows_
 #pragma unroll
             for (int r = 0; r < S0::R; ++r) {
                 const int n = S0::in_n(j, r);
-                float2 z = *reinterpret_cast<const float2 *>(xs + tt * XS + 2 * n);
+                float2 z = tmx ? v[i * S0::R + r] : *reinterpret_cast<const float2 *>(xs + tt * XS + 2 * n);
                 if (mode == 0) {
                     const float2 w = *reinterpret_cast<const float2 *>(wxs + 2 * n);
                     z.x *= w.x;
@@ -524,6 +598,14 @@ __global__ void __launch_bounds__(256, S == 512 ? 4 : S == 1024 ? 2 : 5) k_rows_
                 const float2 m = wr[HP];
                 dst[HP] = r2c_post(m, m, wm);
             }
+        }
+    }
+    if constexpr (TMX_S) {
+        if (tmx) {
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+            __syncthreads();
+            if ((tid >> 5) == 0)
+                asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" :: "r"(tm_slot_x), "n"(64) : "memory");
         }
     }
 }
@@ -834,39 +916,6 @@ __global__ void __launch_bounds__(GC<S>::NTH) k_cols(FftArgs A, int mode, const 
 // shared memory (34 KB less per CTA; measured on c4: H 4.16 -> 4.05 ms, H^T 3.97 ->
 // 3.63 ms).  At 2 CTAs/SM the transform itself still needs 128 registers; forcing 3
 // CTAs/SM (80 registers) spills and is slower (profiles/r1/SUMMARY.md).
-__device__ __forceinline__ void tm_st32(uint32_t ta, const uint32_t (&r)[32]) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%32], {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31};\n" :: "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]), "r"(ta) : "memory");
-}
-__device__ __forceinline__ void tm_ld32(uint32_t ta, uint32_t (&r)[32]) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]) : "r"(ta) : "memory");
-}
-__device__ __forceinline__ void tm_st16(uint32_t ta, const uint32_t (&r)[16]) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%16], {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15};\n" :: "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(ta) : "memory");
-}
-__device__ __forceinline__ void tm_ld16(uint32_t ta, uint32_t (&r)[16]) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];\n" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]) : "r"(ta) : "memory");
-}
-__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
-__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
-
-// E = 16 complex per thread <-> 32 TMEM columns
-template <int E>
-__device__ __forceinline__ void tm_put(uint32_t ta, const float2 (&v)[E]) {
-    static_assert(E == 16, "TMEM column pass holds 16 complex per thread");
-    uint32_t r[32];
-#pragma unroll
-    for (int e = 0; e < E; ++e) { r[2 * e] = __float_as_uint(v[e].x); r[2 * e + 1] = __float_as_uint(v[e].y); }
-    tm_st32(ta, r);
-}
-template <int E>
-__device__ __forceinline__ void tm_get(uint32_t ta, float2 (&v)[E]) {
-    uint32_t r[32];
-    tm_ld32(ta, r);
-    tm_wait_ld();
-#pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = make_float2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1]));
-}
-
 // Twiddle provider of the TMEM column pass (S = 512, stages 1 and 2 with Ns = 8, 64, two
 // butterflies per thread each): w^1..w^7 of the thread's butterfly i of that stage in 16
 // TMEM columns at base + (slot * 2 + i) * 16, written once per CTA from TwTable (same
@@ -1544,10 +1593,11 @@ bool fft_prefer(int P) {
 }
 
 template <int S>
-static size_t smem_rows_fwd(int mode = 0) {
+static size_t smem_rows_fwd(int mode, bool tmx) {
     using G = GR<S>;
-    return (size_t)ROWS_TW(S) * 8 + (size_t)G::NB * G::RS * 8 +
-           ((S == 512 && mode != 0) ? 0 : (size_t)G::NB * G::XS * 4 + (size_t)S * 4);
+    if (S == 512 && mode != 0) return (size_t)ROWS_TW(S) * 8 + (size_t)G::NB * G::RS * 8;
+    if (tmx) return (size_t)ROWS_TW(S) * 8 + (size_t)G::NB * G::RS * 8 + (size_t)S * 4;
+    return (size_t)ROWS_TW(S) * 8 + (size_t)G::NB * G::RS * 8 + (size_t)G::NB * G::XS * 4 + (size_t)S * 4;
 }
 template <int S>
 static size_t smem_cols(int NP, int NQ) {
@@ -1578,7 +1628,9 @@ template <int S>
 static cudaError_t setup_attrs(int T, int NP, int NQ) {
     cudaError_t e;
     (void)T;
-    if ((e = raise_smem(k_rows_fwd<S>, smem_rows_fwd<S>())) != cudaSuccess) return e;
+    if ((e = raise_smem(k_rows_fwd<S, false>, smem_rows_fwd<S>(0, false))) != cudaSuccess) return e;
+    if constexpr (S == 512 && ROWS_FWD_TMEM)
+        if ((e = raise_smem(k_rows_fwd<S, true>, smem_rows_fwd<S>(0, true))) != cudaSuccess) return e;
     if ((e = raise_smem(k_cols<S>, smem_cols<S>(NP, NQ))) != cudaSuccess) return e;
 #if COLS_TMEM
     if constexpr (S == 512)
@@ -1592,7 +1644,13 @@ template <int S>
 static cudaError_t run_rows_fwd(const FftArgs &a, int ntiles, int mode, int par, const float *psfs, int npsf,
                                 float2 *hrows, cudaStream_t s) {
     if (ntiles == 0) return cudaSuccess;
-    k_rows_fwd<S><<<ntiles * (S / GR<S>::NB), GR<S>::NTH, smem_rows_fwd<S>(mode), s>>>(a, mode, par, psfs, npsf, hrows);
+    if constexpr (S == 512 && ROWS_FWD_TMEM) {
+        if (mode == 0) {
+            k_rows_fwd<S, true><<<ntiles * (S / GR<S>::NB), GR<S>::NTH, smem_rows_fwd<S>(mode, true), s>>>(a, mode, par, psfs, npsf, hrows);
+            return cudaGetLastError();
+        }
+    }
+    k_rows_fwd<S, false><<<ntiles * (S / GR<S>::NB), GR<S>::NTH, smem_rows_fwd<S>(mode, false), s>>>(a, mode, par, psfs, npsf, hrows);
     return cudaGetLastError();
 }
 template <int S>
