@@ -57,6 +57,9 @@
 #ifndef ROWS_FWD_TMEM
 #define ROWS_FWD_TMEM 1    // R2C pass (H, S = 512): stage-0 inputs stashed in TMEM, xs aliases work
 #endif
+#ifndef ROWS_INV_HT_TMEM
+#define ROWS_INV_HT_TMEM 1 // H^T C2R pass (S = 512): accumulator in TMEM, 3 CTAs/SM
+#endif
 #ifndef COLS_TM_NYQ
 #define COLS_TM_NYQ 1      // TMEM column pass: Nyquist column packed into column 0 (32 chunks, not 33)
 #endif
@@ -1330,7 +1333,11 @@ struct C2R {
 };
 
 template <int S, bool HT>
-__global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
+__global__ void __launch_bounds__(256, S == 1024 ? (HT ? 1 : 2) : (HT && S == 512 && ROWS_INV_HT_TMEM) ? 3 : 4)
+k_rows_inv(FftArgs A, int mode) {
+    // H^T at S = 512: the accumulator sum_q wx_q C2R(B_q) lives in TMEM (32 columns per
+    // thread) instead of 32 registers, so 3 CTAs/SM fit
+    constexpr bool HTT = HT && S == 512 && ROWS_INV_HT_TMEM;
     using G = GR<S>;
     using C = C2R<S>;
     using F = typename G::F;
@@ -1374,10 +1381,23 @@ __global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
     }
     if (nq > 0) C::issue(stg, src(0), nrows, tid);
     for (int i = tid; i < ROWS_TW(S); i += G::NTH) Wsm[i] = A.W[i];
-    float2 acc[HT ? E : 1];
+    float2 acc[(HT && !HTT) ? E : 1];
 #pragma unroll
-    for (int e = 0; e < (HT ? E : 1); ++e) acc[e] = make_float2(0.f, 0.f);
+    for (int e = 0; e < ((HT && !HTT) ? E : 1); ++e) acc[e] = make_float2(0.f, 0.f);
     float2 v[E];
+    __shared__ uint32_t tm_slot_a;
+    uint32_t t_a = 0;
+    if constexpr (HTT) {
+        if ((tid >> 5) == 0) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
+                         :: "r"((uint32_t)__cvta_generic_to_shared(&tm_slot_a)), "n"(64) : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        t_a = tm_slot_a + ((uint32_t)(32 * ((tid >> 5) & 3)) << 16) + (uint32_t)((tid >> 7) * 32);
+    }
     for (int qi = 0; qi < nq; ++qi) {
         __pipeline_wait_prior(0);
         __syncthreads();
@@ -1390,6 +1410,25 @@ __global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
         if constexpr (HT) {
             // g += wx_q . C2R(B_q): z[n] = (x[2n], x[2n+1]) at the last-stage positions
             const float *wq = wxs + qi * S;
+            if constexpr (HTT) {
+                uint32_t a[32];
+                if (qi > 0) { tm_ld32(t_a, a); tm_wait_ld(); }
+#pragma unroll
+                for (int i = 0; i < SL::BPT; ++i) {
+                    int tt, j;
+                    SL::bj(i, tid, tt, j);
+#pragma unroll
+                    for (int r = 0; r < SL::R; ++r) {
+                        const float2 w = *reinterpret_cast<const float2 *>(wq + 2 * SL::out_n(j, r));
+                        const int e = 2 * (i * SL::R + r);
+                        const float ox = qi > 0 ? __uint_as_float(a[e]) : 0.f, oy = qi > 0 ? __uint_as_float(a[e + 1]) : 0.f;
+                        a[e] = __float_as_uint(ox + w.x * v[i * SL::R + r].x);
+                        a[e + 1] = __float_as_uint(oy + w.y * v[i * SL::R + r].y);
+                    }
+                }
+                tm_st32(t_a, a);
+                tm_wait_st();
+            } else {
 #pragma unroll
             for (int i = 0; i < SL::BPT; ++i) {
                 int tt, j;
@@ -1402,9 +1441,13 @@ __global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
                     o.y += w.y * v[i * SL::R + r].y;
                 }
             }
+            }
         }
     }
     // last-stage values -> outs (aliases work: middle() ended with a barrier)
+    if constexpr (HTT) {
+        if (nq > 0) tm_get<E>(t_a, v);
+    }
 #pragma unroll
     for (int i = 0; i < SL::BPT; ++i) {
         int tt, j;
@@ -1412,13 +1455,18 @@ __global__ void __launch_bounds__(256) k_rows_inv(FftArgs A, int mode) {
 #pragma unroll
         for (int r = 0; r < SL::R; ++r) {
             float2 val;
-            if constexpr (HT) val = acc[i * SL::R + r];
+            if constexpr (HT && !HTT) val = acc[i * SL::R + r];
             else val = v[i * SL::R + r];
             if (nq == 0) val = make_float2(0.f, 0.f);
             *reinterpret_cast<float2 *>(outs + tt * XS + 2 * SL::out_n(j, r)) = val;
         }
     }
+    if constexpr (HTT) asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
+    if constexpr (HTT) {
+        if ((tid >> 5) == 0)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" :: "r"(tm_slot_a), "n"(64) : "memory");
+    }
 
     // valid outputs of this row block: rows [0, nr), columns [0, nc) (facet edge and
     // strip clip); the flat index walks (rr, cc) incrementally (no per-element division)
