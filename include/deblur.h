@@ -65,7 +65,7 @@ extern "C" {
 #define DEBLUR_API
 #endif
 
-#define DEBLUR_ABI_VERSION 2
+#define DEBLUR_ABI_VERSION 3
 
 typedef struct deblur_ctx *deblur_t;
 
@@ -149,6 +149,15 @@ typedef struct {
                                      10 + 10k); eager launches (host-side line-search decisions); at most
                                      64 facets per rank */
     int32_t inner_increment;      /* >= 0, VMLM-B budget increment per outer iteration */
+    int32_t loopback_world;       /* world == 1 only; 0 or 1: off.  V > 1: the facets are assigned to V
+                                     VIRTUAL ranks by the same GPU-grid planner as a world-V run, and
+                                     every band shared by facets of different virtual ranks takes the
+                                     multi-rank path of a5/a6 (Fig. 2): packed
+                                     into per-message send buffers, moved into the matching receive
+                                     buffers (a device copy stands in for ncclSend/ncclRecv) and read
+                                     by the consensus kernel from there.  Results are bitwise equal
+                                     to V = 1 (ascending facet id, A9).  V must factor
+                                     into a GPU grid dividing the facet grid (else DEBLUR_ESHAPE). */
 } deblur_params;
 
 /* 128-byte NCCL unique id for a world > 1 run: call on rank 0, broadcast
@@ -199,6 +208,11 @@ DEBLUR_API deblur_status deblur_get_image(deblur_t h, float *x);
 DEBLUR_API deblur_status deblur_state_size(deblur_t h, int64_t *n_floats);
 DEBLUR_API deblur_status deblur_get_state(deblur_t h, float *x_facets, float *u_facets);
 DEBLUR_API deblur_status deblur_set_state(deblur_t h, const float *x_facets, const float *u_facets);
+/* Outer-iteration counter k of the run (Algorithm 1's loop index), which sets the
+ * VMLM-B inner budget inner_steps + k * inner_increment.  A checkpoint stores it
+ * next to (x_f, u_f); set restores it (k >= 0, else DEBLUR_EINVAL).  deblur_reset sets 0. */
+DEBLUR_API deblur_status deblur_get_outer_iteration(deblur_t h, int32_t *k);
+DEBLUR_API deblur_status deblur_set_outer_iteration(deblur_t h, int32_t k);
 
 /* New observation with the same geometry and PSFs (e.g. the next exposure):
  * upload y (host [M_y][M_x]) and restart from x0 (host [N_y][N_x] or NULL ->

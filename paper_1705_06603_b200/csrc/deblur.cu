@@ -51,6 +51,7 @@ struct SendRecv {
     Message m;
     float *vbuf = nullptr;   // device buffer for v band
     float *xbuf = nullptr;   // device buffer for x band (objective)
+    int peer_index = -1;     // loopback transport: index of the matching receive (sends only)
 };
 
 }  // namespace
@@ -60,6 +61,16 @@ struct deblur_ctx {
     Plan plan;
     int rank = 0, world = 1, device = 0;
     cudaStream_t stream = nullptr;
+    // consensus stream (§8e): the halo exchange and K5 of iteration k run here, under
+    // the H / H^T passes of iteration k+1 (which read only x); the first kernel of
+    // iteration k+1 that reads u waits for ev_cons
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t ev_upd = nullptr, ev_cons = nullptr;
+    bool cons_pending = false;
+    // loopback transport (params.loopback_world = V > 1, world == 1): virtual owner of
+    // every facet under a world-V plan; bands between virtual ranks use send / recv buffers
+    int vworld = 1;
+    std::vector<int> vowner;
     std::vector<int> local;               // facet ids owned by this rank (ascending)
     std::vector<int> local_index;         // facet id -> local index or -1
     std::vector<FacetDev> fh;             // host copies of the descriptors
@@ -150,19 +161,20 @@ struct deblur_ctx {
         if (!ev_pool.empty()) { cudaEvent_t e = ev_pool.back(); ev_pool.pop_back(); return e; }
         cudaEvent_t e; cudaEventCreate(&e); return e;
     }
-    void prof_begin(int cls, cudaEvent_t *a) {
+    void prof_begin(int cls, cudaEvent_t *a, cudaStream_t st = nullptr) {
         if (!prof) return;
         *a = get_event();
-        cudaEventRecord(*a, stream);
+        cudaEventRecord(*a, st ? st : stream);
         (void)cls;
     }
-    void prof_end(int cls, cudaEvent_t a) {
+    void prof_end(int cls, cudaEvent_t a, cudaStream_t st = nullptr) {
         stat_n[cls] += 1;
         if (!prof) return;
         cudaEvent_t b = get_event();
-        cudaEventRecord(b, stream);
+        cudaEventRecord(b, st ? st : stream);
         pending.push_back({cls, a, b});
     }
+    double *d_objbuf = nullptr;           // world > 1: objective all-reduce buffer (2F + 1 doubles)
     void prof_collect() {
         for (auto &p : pending) {
             float ms = 0.f;
@@ -225,6 +237,8 @@ deblur_status validate(const deblur_params *p, std::string &err) {
     if (p->independent != 0 && p->independent != 1) { err = "independent must be 0 or 1"; return DEBLUR_EINVAL; }
     if (p->local_solver != 0 && p->local_solver != 1) { err = "local_solver must be 0 (projected gradient) or 1 (VMLM-B)"; return DEBLUR_EINVAL; }
     if (p->inner_increment < 0) { err = "inner_increment must be >= 0"; return DEBLUR_EINVAL; }
+    if (p->loopback_world < 0) { err = "loopback_world must be >= 0"; return DEBLUR_EINVAL; }
+    if (p->loopback_world > 1 && p->world > 1) { err = "loopback_world needs world == 1"; return DEBLUR_EINVAL; }
     if (p->operator_mode != DEBLUR_OP_INTERP && p->operator_mode != DEBLUR_OP_PER_NODE) {
         err = "operator_mode must be 0 (interpolated H) or 1 (per-node PSFs)";
         return DEBLUR_EINVAL;
@@ -385,32 +399,54 @@ static deblur_status check_state(deblur_t h) {
     return DEBLUR_OK;
 }
 
-// halo exchange: v bands (which == 0) or x[par] bands (which == 1)
-static deblur_status exchange(deblur_t h, int which) {
-    if (h->world == 1 || (h->sends.empty() && h->recvs.empty())) return DEBLUR_OK;
+// halo exchange (a5): v bands (which == 0) or x[par] bands (which == 1)
+// of every band shared with a facet of another rank, on stream `st`: pack each
+// message's rectangle into its contiguous send buffer, then one grouped NCCL
+// send/recv round (world > 1) or, for the loopback transport (one process, virtual
+// ranks), a device copy of each send buffer into the matching receive buffer.
+static deblur_status exchange(deblur_t h, int which, cudaStream_t st) {
+    if (h->sends.empty() && h->recvs.empty()) return DEBLUR_OK;
     cudaEvent_t ev = nullptr;
-    h->prof_begin(KC_XCHG, &ev);
+    h->prof_begin(KC_XCHG, &ev, st);
     for (auto &s : h->sends) {
         const FacetDev &F = h->fh[h->local_index[s.m.src_facet]];
         const float *src = which == 0 ? F.v : F.x[h->par];
         const int64_t w = s.m.rect.x1 - s.m.rect.x0, hh = s.m.rect.y1 - s.m.rect.y0;
         const float *p = src + (s.m.rect.y0 - F.ey0) * F.ep + (s.m.rect.x0 - F.ex0);
         CU(cudaMemcpy2DAsync(which == 0 ? s.vbuf : s.xbuf, w * 4, p, F.ep * 4, w * 4, hh, cudaMemcpyDeviceToDevice,
-                             h->stream));
+                             st));
     }
-    NC(ncclGroupStart(), "halo group start", -1);
-    for (auto &s : h->sends)
-        NC(ncclSend(which == 0 ? s.vbuf : s.xbuf, (size_t)s.m.rect.area(), ncclFloat, s.m.peer, h->comm, h->stream),
-           "halo send", s.m.peer);
-    for (auto &r : h->recvs)
-        NC(ncclRecv(which == 0 ? r.vbuf : r.xbuf, (size_t)r.m.rect.area(), ncclFloat, r.m.peer, h->comm, h->stream),
-           "halo recv", r.m.peer);
-    NC(ncclGroupEnd(), "halo group end", -1);
-    h->prof_end(KC_XCHG, ev);
+    if (h->world > 1) {
+        NC(ncclGroupStart(), "halo group start", -1);
+        for (auto &s : h->sends)
+            NC(ncclSend(which == 0 ? s.vbuf : s.xbuf, (size_t)s.m.rect.area(), ncclFloat, s.m.peer, h->comm, st),
+               "halo send", s.m.peer);
+        for (auto &r : h->recvs)
+            NC(ncclRecv(which == 0 ? r.vbuf : r.xbuf, (size_t)r.m.rect.area(), ncclFloat, r.m.peer, h->comm, st),
+               "halo recv", r.m.peer);
+        NC(ncclGroupEnd(), "halo group end", -1);
+    } else {
+        for (auto &s : h->sends) {
+            const SendRecv &r = h->recvs[s.peer_index];
+            CU(cudaMemcpyAsync(which == 0 ? r.vbuf : r.xbuf, which == 0 ? s.vbuf : s.xbuf,
+                               (size_t)s.m.rect.area() * 4, cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    h->prof_end(KC_XCHG, ev, st);
+    return DEBLUR_OK;
+}
+
+// the stream waits for the consensus (K5) of the previous iteration, if one is pending
+static deblur_status join_consensus(deblur_t h) {
+    if (!h->cons_pending) return DEBLUR_OK;
+    CU(cudaStreamWaitEvent(h->stream, h->ev_cons, 0));
+    h->cons_pending = false;
     return DEBLUR_OK;
 }
 
 static deblur_status finish(deblur_t h) {
+    deblur_status js = join_consensus(h);
+    if (js != DEBLUR_OK) return js;
     CU(cudaStreamSynchronize(h->stream));
     CU(cudaGetLastError());
     if (h->comm) {
@@ -467,6 +503,7 @@ static deblur_status local_step(deblur_t h, int last) {
         deblur_status st;
         if ((st = run_fft_H(h, h->d_facets, h->par, FFT_RESIDUAL)) != DEBLUR_OK) return st;
         if ((st = run_fft_HT(h, h->d_facets)) != DEBLUR_OK) return st;
+        if ((st = join_consensus(h)) != DEBLUR_OK) return st;          // K4 reads u
         h->prof_begin(KC_UPDATE_G, &ev);
         CU(launch_update_from_g(h->d_facets, h->d_tilesHT, (int)h->tilesHT.size(), h->plan.P, h->par, last, h->sc,
                                 nullptr, h->stream));
@@ -475,6 +512,8 @@ static deblur_status local_step(deblur_t h, int last) {
         h->prof_begin(KC_H, &ev);
         CU(launch_H_direct(h->conv_args(h->d_facets, false), H_RESIDUAL, h->par, h->stream));
         h->prof_end(KC_H, ev);
+        deblur_status st = join_consensus(h);                          // K2's epilogue reads u
+        if (st != DEBLUR_OK) return st;
         h->prof_begin(KC_HT_UPDATE, &ev);
         CU(launch_HT_direct(h->conv_args(h->d_facets, true), HT_UPDATE, h->par, last, h->sc, h->stream));
         h->prof_end(KC_HT_UPDATE, ev);
@@ -543,6 +582,7 @@ deblur_status deblur_destroy(deblur_t h) {
     if (!h) return DEBLUR_OK;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->cstream) cudaStreamSynchronize(h->cstream);
     for (auto &g : h->gexec)
         if (g) { cudaGraphExecDestroy(g); g = nullptr; }
     if (h->fft) { fft_destroy(h->fft); h->fft = nullptr; }
@@ -551,6 +591,9 @@ deblur_status deblur_destroy(deblur_t h) {
     for (auto &p : h->pending) { h->ev_pool.push_back(p.a); h->ev_pool.push_back(p.b); }
     for (auto e : h->ev_pool) cudaEventDestroy(e);
     for (void *p : h->allocs) cudaFree(p);
+    if (h->ev_upd) cudaEventDestroy(h->ev_upd);
+    if (h->ev_cons) cudaEventDestroy(h->ev_cons);
+    if (h->cstream) cudaStreamDestroy(h->cstream);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
     return DEBLUR_OK;
@@ -572,6 +615,14 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
     if (!err.empty()) { g_last_error = err; return DEBLUR_ESHAPE; }
     const Plan &pl = h->plan;
     const int P = pl.P;
+    Plan vplan;                           // loopback transport: the world-V plan of the virtual ranks
+    h->vowner.assign(pl.facets.size(), h->rank);
+    if (p->world == 1 && p->loopback_world > 1) {
+        err = make_plan(p->ny, p->nx, p->psf_size, p->facet_gy, p->facet_gx, p->overlap, p->loopback_world, vplan);
+        if (!err.empty()) { g_last_error = "loopback_world: " + err; return DEBLUR_ESHAPE; }
+        h->vworld = p->loopback_world;
+        for (const auto &f : vplan.facets) h->vowner[f.id] = f.owner;
+    }
     h->per_node = p->operator_mode == DEBLUR_OP_PER_NODE;
     if (h->per_node) {
         err = check_node_weights(pl, p->interp_wy, p->interp_wx);
@@ -601,6 +652,9 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
     } while (0)
     CUC(cudaSetDevice(p->device));
     CUC(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    CUC(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
+    CUC(cudaEventCreateWithFlags(&h->ev_upd, cudaEventDisableTiming));
+    CUC(cudaEventCreateWithFlags(&h->ev_cons, cudaEventDisableTiming));
 
     // conv path (A: measured crossover)
     int path = p->conv_path;
@@ -681,6 +735,19 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
     if (h->world > 1) {
         for (auto &m : messages_from(pl, h->rank)) { SendRecv s; s.m = m; h->sends.push_back(s); }
         for (auto &m : messages_to(pl, h->rank)) { SendRecv s; s.m = m; h->recvs.push_back(s); }
+    } else if (h->vworld > 1) {
+        for (int vr = 0; vr < h->vworld; ++vr) {
+            for (auto &m : messages_from(vplan, vr)) { SendRecv s; s.m = m; h->sends.push_back(s); }
+            for (auto &m : messages_to(vplan, vr)) { SendRecv s; s.m = m; h->recvs.push_back(s); }
+        }
+        for (auto &s : h->sends)
+            for (size_t i = 0; i < h->recvs.size(); ++i)
+                if (h->recvs[i].m.src_facet == s.m.src_facet && h->recvs[i].m.dst_facet == s.m.dst_facet)
+                    s.peer_index = (int)i;
+        for (auto &s : h->sends)
+            if (s.peer_index < 0) { g_last_error = "loopback: unmatched halo message"; return DEBLUR_ESHAPE; }
+    }
+    {
         for (auto *lst : {&h->sends, &h->recvs})
             for (auto &s : *lst) {
                 CUC(h->dalloc(&s.vbuf, (size_t)s.m.rect.area()));
@@ -700,7 +767,7 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
                 nb.ay = axisw(np.ey0, np.ey1, np.py_e, np.ny_s, node_wy(np));
                 nb.ax = axisw(np.ex0, np.ex1, np.px_e, np.nx_s, node_wx(np));
                 const int nli = h->local_index[np.id];
-                if (nli >= 0) {
+                if (nli >= 0 && h->vowner[np.id] == h->vowner[F.id]) {     // same (virtual) rank: direct read
                     const FacetDev &N = (nli == (int)li) ? F : h->fh[nli];
                     nb.v.base[0] = nb.v.base[1] = N.v;
                     nb.v.pitch = N.ep; nb.v.y0 = N.ey0; nb.v.x0 = N.ex0; nb.v.valid = 1;
@@ -861,6 +928,7 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
 
     // NCCL
     if (h->world > 1) {
+        CUC(h->dalloc(&h->d_objbuf, 2 * pl.facets.size() + 1));
         ncclUniqueId id;
         std::memcpy(&id, p->nccl_id, sizeof id);
         ncclResult_t r = ncclCommInitRank(&h->comm, h->world, id, h->rank);
@@ -1110,6 +1178,8 @@ static deblur_status vm_local_solve(deblur_t h) {
 static deblur_status one_iteration(deblur_t h) {
     deblur_status s;
     if (h->vm.on) {
+        if ((s = join_consensus(h)) != DEBLUR_OK) return s;
+
         if ((s = vm_local_solve(h)) != DEBLUR_OK) return s;
         ++h->vm.k_outer;
         if (!h->prm.independent) {     // what the last projected-gradient step's epilogue writes
@@ -1122,12 +1192,18 @@ static deblur_status one_iteration(deblur_t h) {
             if ((s = local_step(h, k == h->prm.inner_steps - 1 && !h->prm.independent)) != DEBLUR_OK) return s;
     }
     if (h->prm.independent) return DEBLUR_OK;        // baseline: no exchange, no consensus
-    if ((s = exchange(h, 0)) != DEBLUR_OK) return s;
+    // a5 + a6 on the consensus stream: they need x+ and v of this iteration; the next
+    // iteration's H / H^T passes (x only) run under them (§8e)
+    CU(cudaEventRecord(h->ev_upd, h->stream));
+    CU(cudaStreamWaitEvent(h->cstream, h->ev_upd, 0));
+    if ((s = exchange(h, 0, h->cstream)) != DEBLUR_OK) return s;
     cudaEvent_t ev = nullptr;
-    h->prof_begin(KC_CONSENSUS, &ev);
+    h->prof_begin(KC_CONSENSUS, &ev, h->cstream);
     CU(launch_consensus(h->d_facets, h->d_rects, h->d_rect_tiles, (int)h->rect_tiles.size(), h->par, h->sc.rho,
-                        h->stream));
-    h->prof_end(KC_CONSENSUS, ev);
+                        h->cstream));
+    h->prof_end(KC_CONSENSUS, ev, h->cstream);
+    CU(cudaEventRecord(h->ev_cons, h->cstream));
+    h->cons_pending = true;
     return DEBLUR_OK;
 }
 
@@ -1140,6 +1216,7 @@ static deblur_status capture_pair(deblur_t h) {
     CU(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeRelaxed));
     deblur_status s = one_iteration(h);
     if (s == DEBLUR_OK) s = one_iteration(h);
+    if (s == DEBLUR_OK) s = join_consensus(h);            // the forked consensus stream rejoins
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(h->stream, &g);
     if (s != DEBLUR_OK) { if (g) cudaGraphDestroy(g); return s; }
@@ -1167,6 +1244,7 @@ deblur_status deblur_iterate(deblur_t h, int32_t n) {
     }
     for (; done < n; ++done)
         if ((s = one_iteration(h)) != DEBLUR_OK) return s;
+    if ((s = join_consensus(h)) != DEBLUR_OK) return s;    // callers time on h->stream
     return finish(h);
 }
 
@@ -1219,7 +1297,8 @@ deblur_status deblur_objective(deblur_t h, double out[4]) {
                        h->stream));
     CU(cudaStreamSynchronize(h->stream));
     for (size_t t = 0; t < h->tilesHT.size(); ++t) reg[h->local[h->tilesHT[t].f]] += h->h_partials[t];
-    if ((s = exchange(h, 1)) != DEBLUR_OK) return s;
+    if ((s = join_consensus(h)) != DEBLUR_OK) return s;
+    if ((s = exchange(h, 1, h->stream)) != DEBLUR_OK) return s;
     h->prof_begin(KC_MAXDIFF, &ev);
     CU(launch_maxdiff(h->d_facets, h->d_rects, (int)h->rects.size(), h->par, h->d_partials, h->stream));
     h->prof_end(KC_MAXDIFF, ev);
@@ -1229,12 +1308,11 @@ deblur_status deblur_objective(deblur_t h, double out[4]) {
     for (size_t r = 0; r < h->rects.size(); ++r) md = std::max(md, h->h_partials[r]);
     if (h->world > 1) {
         // per-facet values are nonzero only on their owner: a sum all-reduce is exact
-        double *d = nullptr;
-        CU(h->dalloc(&d, 2 * F + 1));
+        double *d = h->d_objbuf;              // allocated once in deblur_create
         std::vector<double> buf(2 * F + 1);
         for (int f = 0; f < F; ++f) { buf[f] = data[f]; buf[F + f] = reg[f]; }
         buf[2 * F] = md;
-        CU(cudaMemcpy(d, buf.data(), sizeof(double) * (2 * F + 1), cudaMemcpyHostToDevice));
+        CU(cudaMemcpyAsync(d, buf.data(), sizeof(double) * (2 * F + 1), cudaMemcpyHostToDevice, h->stream));
         NC(ncclAllReduce(d, d, 2 * F, ncclDouble, ncclSum, h->comm, h->stream), "objective allreduce", -1);
         NC(ncclAllReduce(d + 2 * F, d + 2 * F, 1, ncclDouble, ncclMax, h->comm, h->stream), "objective allreduce", -1);
         CU(cudaMemcpyAsync(buf.data(), d, sizeof(double) * (2 * F + 1), cudaMemcpyDeviceToHost, h->stream));
@@ -1529,6 +1607,19 @@ deblur_status deblur_reset(deblur_t h, const float *y, const float *x0) {
     if ((s = upload_y(h, y)) != DEBLUR_OK) return s;
     h->vm.k_outer = 0;                                // a fresh solve: VMLM-B budget schedule restarts
     return upload_state_x0(h, x0, y);
+}
+
+deblur_status deblur_get_outer_iteration(deblur_t h, int32_t *k) {
+    if (!h || !k) return DEBLUR_EINVAL;
+    *k = h->vm.k_outer;
+    return DEBLUR_OK;
+}
+
+deblur_status deblur_set_outer_iteration(deblur_t h, int32_t k) {
+    if (!h) return DEBLUR_EINVAL;
+    if (k < 0) return h->fail(DEBLUR_EINVAL, "outer iteration must be >= 0");
+    h->vm.k_outer = k;
+    return DEBLUR_OK;
 }
 
 deblur_status deblur_get_step(deblur_t h, double *tau) {

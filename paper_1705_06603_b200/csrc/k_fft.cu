@@ -1388,6 +1388,7 @@ k_rows_inv(FftArgs A, int mode) {
     __shared__ uint32_t tm_slot_a;
     uint32_t t_a = 0;
     if constexpr (HTT) {
+        static_assert(E == 16, "the TMEM accumulator holds 16 complex = 32 columns per thread");
         if ((tid >> 5) == 0) {
             asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
                          :: "r"((uint32_t)__cvta_generic_to_shared(&tm_slot_a)), "n"(64) : "memory");

@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "libdeblur.so")
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 OP_INTERP, OP_PER_NODE = 0, 1
 CONV_AUTO, CONV_DIRECT, CONV_FFT = 0, 1, 2
 STATUS = {0: "DEBLUR_OK", -1: "DEBLUR_EINVAL", -2: "DEBLUR_ESHAPE", -3: "DEBLUR_ENOMEM", -4: "DEBLUR_ECUDA",
@@ -46,6 +46,7 @@ class Params(ctypes.Structure):
         ("operator_mode", ctypes.c_int32),
         ("independent", ctypes.c_int32),
         ("local_solver", ctypes.c_int32), ("inner_increment", ctypes.c_int32),
+        ("loopback_world", ctypes.c_int32),
     ]
 
 
@@ -84,6 +85,8 @@ def lib():
             "deblur_state_size": ([h, _lp], ctypes.c_int),
             "deblur_get_state": ([h, _fp, _fp], ctypes.c_int),
             "deblur_set_state": ([h, _fp, _fp], ctypes.c_int),
+            "deblur_get_outer_iteration": ([h, _ip], ctypes.c_int),
+            "deblur_set_outer_iteration": ([h, ctypes.c_int32], ctypes.c_int),
             "deblur_reset": ([h, _fp, _fp], ctypes.c_int),
             "deblur_get_step": ([h, _dp], ctypes.c_int),
             "deblur_set_profiling": ([h, ctypes.c_int32], ctypes.c_int),
@@ -107,7 +110,8 @@ def lib():
 
 EXPORTED = ["deblur_nccl_id", "deblur_create", "deblur_destroy", "deblur_apply_H", "deblur_apply_HT",
             "deblur_apply_H_device", "deblur_apply_HT_device", "deblur_iterate", "deblur_iterate_traced",
-            "deblur_objective", "deblur_get_image", "deblur_state_size", "deblur_get_state", "deblur_set_state", "deblur_reset",
+            "deblur_objective", "deblur_get_image", "deblur_state_size", "deblur_get_state", "deblur_set_state",
+            "deblur_get_outer_iteration", "deblur_set_outer_iteration", "deblur_reset",
             "deblur_get_step", "deblur_set_profiling", "deblur_kernel_stats", "deblur_kernel_name",
             "deblur_reset_stats", "deblur_kernel_work", "deblur_get_conv_path", "deblur_get_stream", "deblur_plan_facets", "deblur_plan_messages",
             "deblur_last_error"]
@@ -138,7 +142,7 @@ def make_params(psfs, wy, wx, y, noise_w=None, noise_w_scalar: float = 1.0, lam:
                 tau: float = 0.0, inner_steps: int = 1, facet_gy: int = 1, facet_gx: int = 1, overlap: int = 0,
                 x0=None, conv_path: int = CONV_AUTO, rank: int = 0, world: int = 1, device: int = 0,
                 nccl_id_bytes: Optional[bytes] = None, operator_mode: int = 0, independent: int = 0,
-                local_solver: int = 0, inner_increment: int = 0):
+                local_solver: int = 0, inner_increment: int = 0, loopback_world: int = 0):
     """Returns (Params, keepalive) -- keepalive holds the arrays the pointers refer to."""
     psfs = _f32(psfs)
     wy, wx, y = _f32(wy), _f32(wx), _f32(y)
@@ -165,7 +169,7 @@ def make_params(psfs, wy, wx, y, noise_w=None, noise_w_scalar: float = 1.0, lam:
                overlap=overlap, x0=_ptr(x0a), conv_path=conv_path, rank=rank, world=world, device=device,
                nccl_id=ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None,
                operator_mode=operator_mode, independent=int(independent), local_solver=local_solver,
-               inner_increment=inner_increment)
+               inner_increment=inner_increment, loopback_world=loopback_world)
     return p, keep
 
 
@@ -293,8 +297,21 @@ class Deblur:
         return x, u
 
     def set_state(self, x, u):
-        x, u = _f32(x), _f32(u)
+        x, u = _f32(x).ravel(), _f32(u).ravel()
+        n = self.state_size()
+        if x.size != n or u.size != n:
+            raise ValueError(f"set_state: x and u must hold state_size() = {n} floats (got {x.size}, {u.size})")
         self._c(self._lib.deblur_set_state(self._h, _ptr(x), _ptr(u)))
+
+    @property
+    def outer_iteration(self) -> int:
+        k = ctypes.c_int32(0)
+        self._c(self._lib.deblur_get_outer_iteration(self._h, ctypes.byref(k)))
+        return k.value
+
+    @outer_iteration.setter
+    def outer_iteration(self, k: int):
+        self._c(self._lib.deblur_set_outer_iteration(self._h, int(k)))
 
     def reset(self, y, x0=None):
         y = _f32(y)

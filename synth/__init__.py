@@ -27,13 +27,14 @@ PSF jitter, noise] for config k.
 from __future__ import annotations
 
 import dataclasses
+import hashlib
 import math
 from typing import Optional
 
 import numpy as np
 
 __all__ = ["Problem", "CONFIGS", "make_config", "make_problem", "per_node", "hat_weights",
-           "psf_grid", "render_observed", "render_scene"]
+           "psf_grid", "render_observed", "render_scene", "input_hash"]
 
 
 @dataclasses.dataclass
@@ -397,3 +398,21 @@ def per_node(pb: Problem, overlap: Optional[int] = None) -> Problem:
         overlap -= overlap % 2
     return dataclasses.replace(pb, fy=pb.gy, fx=pb.gx, overlap=int(overlap), operator_mode=1,
                                name=pb.name + "-node")
+
+
+def input_hash(pb: Problem) -> str:
+    """sha256 of the exact bytes deblur_create / the oracle consume (PSFs, weights,
+    y, W and the scalar parameters), so stored golden values can be tied to the
+    inputs they were computed from."""
+    h = hashlib.sha256()
+    for a in (pb.psfs, pb.wy, pb.wx, pb.y, pb.noise_w, pb.x0):
+        if a is None:
+            h.update(b"none")
+        else:
+            a = np.ascontiguousarray(a)
+            h.update(str((a.dtype.str, a.shape)).encode())
+            h.update(a.tobytes())
+    h.update(repr((pb.ny, pb.nx, pb.P, pb.gy, pb.gx, float(pb.noise_w_scalar), pb.lam, pb.eps, pb.gamma,
+                   pb.rho, pb.reg_kind, pb.tv_boundary, pb.inner_steps, pb.fy, pb.fx, pb.overlap,
+                   pb.operator_mode, pb.independent, pb.local_solver, pb.inner_increment)).encode())
+    return h.hexdigest()

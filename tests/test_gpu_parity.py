@@ -23,6 +23,18 @@ def rel_l2(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
+def load_state(orc, xs, us):
+    """Put a concatenated (planner-order) facet state into the oracle."""
+    o = 0
+    for i, f in enumerate(orc.facets):
+        n = (f.ey[1] - f.ey[0]) * (f.ex[1] - f.ex[0])
+        shp = (f.ey[1] - f.ey[0], f.ex[1] - f.ex[0])
+        orc.x[i] = np.asarray(xs[o:o + n], np.float64).reshape(shp)
+        orc.u[i] = np.asarray(us[o:o + n], np.float64).reshape(shp)
+        o += n
+    return orc
+
+
 def oracle_op(pb):
     return Operator(pb.psfs, pb.wy, pb.wx)
 
@@ -391,11 +403,20 @@ def test_iterate_vmlmb(k, n, facets, O, budget, inc, iters, path):
         obj = dev.objective()
     orc.iterate(iters)
     xr, ur = orc.state()
+    xr_f, ur_f = [a.copy() for a in orc.x], [a.copy() for a in orc.u]
     assert rel_l2(xs, xr) <= IT_TOL, rel_l2(xs, xr)
     assert rel_l2(us, ur) <= IT_TOL, rel_l2(us, ur)
+    # The objective bar (1e-4) applies to the objective *function* (Eq. (4), A22): the
+    # oracle evaluates it at the GPU's own iterate.  Along the two trajectories the
+    # objectives differ by what the iterates differ by (the L-BFGS fp32 / fp64 drift,
+    # bounded by the iterate bar above; reading V7).
+    at_gpu = load_state(orc, xs, us).objective()
+    for i in range(3):
+        assert abs(obj[i] - at_gpu[i]) <= OBJ_TOL * abs(at_gpu[i]), (i, obj[i], at_gpu[i])
+    orc.x, orc.u = [a.copy() for a in xr_f], [a.copy() for a in ur_f]
     ro = orc.objective()
     for i in range(3):
-        assert abs(obj[i] - ro[i]) <= 10 * OBJ_TOL * abs(ro[i]), (i, obj[i], ro[i])
+        assert abs(obj[i] - ro[i]) <= IT_TOL * abs(ro[i]), (i, obj[i], ro[i])
 
 
 @pytest.mark.parametrize("rem", [193, 194, 195, 60])

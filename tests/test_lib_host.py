@@ -73,6 +73,7 @@ def test_planner_messages_are_pairwise_consistent():
                                                 ("operator_mode", 1, "facet grid"), ("independent", 3, "independent"),
                                                 ("local_solver", 2, "local_solver"),
                                                 ("inner_increment", -1, "inner_increment"),
+                                                ("loopback_world", -1, "loopback_world"),
                                                 ("abi_version", 1, "abi_version")])
 def test_validation_names_argument(field, value, needle):
     params, keep, pb = small_params()
@@ -99,3 +100,16 @@ def test_create_without_gpu_fails_loudly():
     with pytest.raises(D.DeblurError) as ei:
         D.Deblur(params, keep)
     assert ei.value.status == -4       # DEBLUR_ECUDA, never a silent CPU path
+
+
+def test_loopback_world_validation():
+    """loopback_world (the one-process multi-rank path) must factor into a GPU grid of
+    the facet grid, and needs world == 1; both are checked before any device work."""
+    params, keep, pb = small_params(loopback_world=5)          # 2 x 3 facets: no 5-rank grid
+    with pytest.raises(D.DeblurError) as ei:
+        D.Deblur(params, keep)
+    assert ei.value.status == -2 and "loopback_world" in str(ei.value)
+    params, keep, pb = small_params(loopback_world=2, world=2, nccl_id_bytes=b"\0" * 128)
+    with pytest.raises(D.DeblurError) as ei:
+        D.plan_facets(params)
+    assert "loopback_world" in str(ei.value)

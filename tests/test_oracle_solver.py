@@ -176,6 +176,55 @@ def test_local_gradient_matches_fd_of_dense_cost():
             assert fd == pytest.approx(gr[a, b], rel=1e-6, abs=1e-8)
 
 
+@pytest.mark.parametrize("kind,bnd", [(0, 0), (1, 0), (0, 1)])
+def test_local_value_grad_pinned(kind, bnd):
+    """local_value_grad (the function whose value drives VMLM-B's Armijo test,
+    reading V4) against things other than itself: its value equals the prox
+    objective f_i(w) + 1/2 |w - u_i|^2_alpha built from the
+    dense matrix of the paper's operator form; its gradient equals central
+    differences of its own value and the projected-gradient path's local_grad.
+    A dropped 1/2 (data or prox term) or a lost lambda fails the value check."""
+    psfs, wy, wx, y, w, prm, F, O = tiny(lam=0.05, eps=0.2, seed=5, kind=kind, bnd=bnd, w_arr=True)
+    d = Deblur(psfs, wy, wx, y, w, *F, O, prm)
+    A = dense_H(psfs, wy, wx)
+    n = 24
+    M = y.shape[0]
+    rng = np.random.default_rng(6)
+    for i, f in enumerate(d.facets):
+        rows = [a * M + b for a in range(*f.oy) for b in range(*f.ox)]
+        cols = [a * n + b for a in range(*f.ey) for b in range(*f.ex)]
+        Af = A[np.ix_(rows, cols)]
+        yf = y[slice(*f.oy), slice(*f.ox)].ravel()
+        wf = np.broadcast_to(w, y.shape)[slice(*f.oy), slice(*f.ox)].ravel()
+        al = prm.gamma * f.omega()
+        u = rng.uniform(0, 1, f.shape)
+        x = rng.uniform(0, 1, f.shape)
+        res = Af @ x.ravel() - yf
+        # TV term summed per pixel from the closed-form phi of A1 (smoothed TV) or the
+        # paper's Huber (P:279-281) on forward differences (circular or Neumann)
+        if bnd == 0:
+            dy, dx = np.roll(x, -1, 0) - x, np.roll(x, -1, 1) - x
+        else:
+            dy, dx = np.zeros_like(x), np.zeros_like(x)
+            dy[:-1] = x[1:] - x[:-1]
+            dx[:, :-1] = x[:, 1:] - x[:, :-1]
+        t = np.sqrt(dy ** 2 + dx ** 2)
+        if kind == 0:
+            reg = (np.sqrt(t ** 2 + prm.eps ** 2) - prm.eps).sum()
+        else:
+            reg = np.where(t <= prm.eps, 0.5 * t ** 2, prm.eps * (t - 0.5 * prm.eps)).sum()
+        want = 0.5 * (wf * res * res).sum() + prm.lam * reg + 0.5 * (al * (x - u) ** 2).sum()
+        val, g = d.local_value_grad(i, x, u)
+        assert val == pytest.approx(want, rel=1e-12)
+        np.testing.assert_allclose(g, d.local_grad(i, x, u), rtol=1e-12, atol=1e-12)
+        for _ in range(8):
+            a, b = rng.integers(0, f.shape[0]), rng.integers(0, f.shape[1])
+            e = np.zeros_like(x)
+            e[a, b] = 1e-6
+            fd = (d.local_value_grad(i, x + e, u)[0] - d.local_value_grad(i, x - e, u)[0]) / 2e-6
+            assert fd == pytest.approx(g[a, b], rel=1e-6, abs=1e-8)
+
+
 def test_noiseless_truth_is_stationary():
     """lambda = 0, alpha = 0, y = H x* -> residual 0, gradient 0, objective 0."""
     psfs, wy, wx, _, _, prm, F, O = tiny(gamma=0.0)
