@@ -15,7 +15,10 @@ term, A8) depend only on a (4c+1)^2 neighbourhood of x and on u at the pixel:
     u+ = u + rho (x+ - u)
 
 so the oracle recomputes x+ and u+ there exactly (fp64) without a full-size
-solve.  Band pixels are covered at reduced size by test_gpu_parity.py.
+solve.  Band pixels (2- and 4-facet, facet borders) take every facet's own step and
+Lemma 1 (test_iterate_full_size_band_pixels).  One iteration is launched eagerly;
+test_graph_replay_equals_eager_full_size ties it to the CUDA-graph replay bench.py
+times (bitwise).  tests/test_gpu_golden.py holds the multi-iteration full-size runs.
 """
 import numpy as np
 import pytest
@@ -94,7 +97,7 @@ def test_iterate_full_size_sampled(k, count):
     with D.Deblur.from_problem(pb, tau=tau) as dev:
         assert dev.conv_path == D.CONV_FFT                       # the bench's AUTO choice at P >= 7
         dev.set_state(xs, us)
-        dev.iterate(1)                                           # graph replay, as timed by bench.py
+        dev.iterate(1)                                           # eager; == graph replay (test below)
         xg, ug = dev.get_state()
     del xs, us
     rng = np.random.default_rng(k)
@@ -111,6 +114,105 @@ def test_iterate_full_size_sampled(k, count):
         ref_x.append(xp)
         ref_u.append(up)
     assert np.count_nonzero(ref_x) >= len(ref_x) // 2           # the step is not all clipped
+    assert rel_l2(got_x, ref_x) <= IT_TOL, rel_l2(got_x, ref_x)
+    assert rel_l2(got_u, ref_u) <= IT_TOL, rel_l2(got_u, ref_u)
+
+
+def _band_samples(pb, facets, count, rng):
+    """Global estimate pixels shared by >= 2 facets: half on 4-facet corner bands,
+    half on 2-facet edge bands, some on a facet's first/last row or column (where
+    the circular D of A2 wraps around that facet)."""
+    out = []
+    fac_by = {(f.fy, f.fx): f for f in facets}
+    while len(out) < count:
+        f = facets[int(rng.integers(len(facets)))]
+        right = fac_by.get((f.fy, f.fx + 1))
+        down = fac_by.get((f.fy + 1, f.fx))
+        if right is None or down is None:
+            continue
+        kind = len(out) % 3
+        ys = (down.ey[0], f.ey[1])                     # rows of the band with the facet below
+        xs = (right.ex[0], f.ex[1])                    # columns of the band with the facet right
+        if kind == 0:                                  # 4-facet corner band
+            gy, gx = int(rng.integers(*ys)), int(rng.integers(*xs))
+        elif kind == 1:                                # edge band with the facet below
+            gy, gx = int(rng.integers(*ys)), int(rng.integers(f.ex[0] + 4, right.ex[0]))
+        else:                                          # facet border row / column inside a band
+            gy = int(rng.choice([down.ey[0], f.ey[1] - 1]))
+            gx = int(rng.integers(f.ex[0] + 4, right.ex[0]))
+        out.append((gy, gx))
+    return out
+
+
+def _oracle_band_update(pb, op, facets, X, U, tau, gy, gx):
+    """x+_f and u+_f at global estimate pixel l = (gy, gx) for every facet f containing
+    it: the Local-Solver step of each facet from its own data (r_f = 0 outside O_f,
+    circular D on P_f, prox weight gamma omega^F_f; Alg. 1, R1, A2) and
+    the consensus of Lemma 1 (A8/A9, ascending facet id)."""
+    c = op.c
+    y0, x0 = max(0, gy - 2 * c), max(0, gx - 2 * c)
+    y1, x1 = min(pb.my, gy + 1), min(pb.mx, gx + 1)            # observed rows/cols seeing l
+    hx = op.H_window(X[y0:y1 + 2 * c, x0:x1 + 2 * c].astype(np.float64), y0, x0)
+    yw = pb.y[y0:y1, x0:x1].astype(np.float64)
+    w = (pb.noise_w[y0:y1, x0:x1].astype(np.float64) if pb.noise_w is not None
+         else np.float64(np.float32(pb.noise_w_scalar)))
+    r_all = w * (hx - yw)
+    res = []
+    for f in facets:
+        if not (f.ey[0] <= gy < f.ey[1] and f.ex[0] <= gx < f.ex[1]):
+            continue
+        r = r_all.copy()                                       # r_f: zero outside O_f
+        ii = np.arange(y0, y1)[:, None]
+        jj = np.arange(x0, x1)[None, :]
+        r[~((ii >= f.oy[0]) & (ii < f.oy[1]) & (jj >= f.ox[0]) & (jj < f.ox[1]))] = 0.0
+        g = op.HT_window(r, y0, x0)[gy - y0, gx - x0]
+        ly, lx = gy - f.ey[0], gx - f.ex[0]
+        ny, nx = f.shape
+        rows = (np.arange(ly - 2, ly + 3) % ny) + f.ey[0]      # circular D within the facet
+        cols = (np.arange(lx - 2, lx + 3) % nx) + f.ex[0]
+        t = tv.grad(X[np.ix_(rows, cols)].astype(np.float64), pb.eps, pb.reg_kind, pb.tv_boundary)[2, 2]
+        om = float(f.wy[ly] * f.wx[lx])
+        xv, uv = float(X[gy, gx]), float(U[gy, gx])
+        xp = max(0.0, xv - tau * (g + pb.lam * t + pb.gamma * om * (xv - uv)))
+        res.append((f.id, om, xp, uv))
+    num = sum(om * (2 * xp - uv) for _, om, xp, uv in res)     # ascending facet id
+    den = sum(om for _, om, _, _ in res)
+    zbar = num / den
+    return [(fid, xp, uv + pb.rho * (zbar - xp)) for fid, _, xp, uv in res]
+
+
+@pytest.mark.parametrize("k,count", [(4, 18), (5, 12)], ids=["c4", "c5"])
+def test_iterate_full_size_band_pixels(k, count):
+    """One full distributed iteration at BASELINE size at band pixels (shared by 2 or 4
+    facets, including facet-border rows where D wraps): x+ of every facet containing the
+    pixel from its own facet-local data, then Lemma 1 and the dual update, against the
+    GPU state in bench.py's launch configuration."""
+    pb = synth.make_config(k)
+    facets = geometry.plan(pb.ny, pb.nx, pb.P, pb.fy, pb.fx, pb.overlap)
+    w_max = float(pb.noise_w.max()) if pb.noise_w is not None else float(np.float32(pb.noise_w_scalar))
+    tau = solver.default_tau(pb.psfs, pb.wy, pb.wx, w_max, pb.lam, pb.eps, pb.reg_kind, pb.gamma)
+    X, U, xs, us = _state(pb, facets, seed=200 + k)
+    with D.Deblur.from_problem(pb, tau=tau) as dev:
+        dev.set_state(xs, us)
+        dev.iterate(1)                                   # eager; == graph replay (test below)
+        xg, ug = dev.get_state()
+    del xs, us
+    rng = np.random.default_rng(300 + k)
+    pix = _band_samples(pb, facets, count, rng)
+    offs = np.cumsum([0] + [(f.ey[1] - f.ey[0]) * (f.ex[1] - f.ex[0]) for f in facets])
+    op = Operator(pb.psfs, pb.wy, pb.wx)
+    got_x, got_u, ref_x, ref_u, nshared = [], [], [], [], []
+    for gy, gx in pix:
+        out = _oracle_band_update(pb, op, facets, X, U, tau, gy, gx)
+        nshared.append(len(out))
+        for fid, xp, up in out:
+            f = facets[fid]
+            o = offs[fid] + (gy - f.ey[0]) * (f.ex[1] - f.ex[0]) + (gx - f.ex[0])
+            got_x.append(xg[o])
+            got_u.append(ug[o])
+            ref_x.append(xp)
+            ref_u.append(up)
+    assert min(nshared) >= 2 and max(nshared) == 4
     assert rel_l2(got_x, ref_x) <= IT_TOL, rel_l2(got_x, ref_x)
     assert rel_l2(got_u, ref_u) <= IT_TOL, rel_l2(got_u, ref_u)
 
@@ -177,3 +279,23 @@ def test_paper_shaped_c6_iterate_small():
     ro = orc.objective()
     for i in range(3):
         assert abs(obj[i] - ro[i]) <= 1e-4 * abs(ro[i]), (i, obj[i], ro[i])
+
+
+@pytest.mark.parametrize("k", [4, 5])
+def test_graph_replay_equals_eager_full_size(k, monkeypatch):
+    """The CUDA-graph replay of deblur_iterate (bench.py's launch configuration) and
+    eager launches give bitwise identical states at full size."""
+    pb = synth.make_config(k)
+    facets = geometry.plan(pb.ny, pb.nx, pb.P, pb.fy, pb.fx, pb.overlap)
+    _, _, xs, us = _state(pb, facets, seed=400 + k)
+    with D.Deblur.from_problem(pb) as dev:
+        dev.set_state(xs, us)
+        dev.iterate(2)
+        xa, ua = dev.get_state()
+    monkeypatch.setenv("DEBLUR_NO_GRAPHS", "1")
+    with D.Deblur.from_problem(pb) as dev:
+        dev.set_state(xs, us)
+        dev.iterate(2)
+        xb, ub = dev.get_state()
+    np.testing.assert_array_equal(xa, xb)
+    np.testing.assert_array_equal(ua, ub)
