@@ -63,6 +63,12 @@
 #ifndef COLS_TM_NYQ
 #define COLS_TM_NYQ 1      // TMEM column pass: Nyquist column packed into column 0 (32 chunks, not 33)
 #endif
+#ifndef COLS_TM_OPEN
+#define COLS_TM_OPEN 1     // TMEM column pass: no barrier after a transform's last exchange (callers sync)
+#endif
+#ifndef COLS_TM_TWPRE
+#define COLS_TM_TWPRE 1    // TMEM column pass: a stage's twiddles loaded from TMEM before the exchange barrier
+#endif
 #ifndef COLS_TM_MINB
 #define COLS_TM_MINB (16 / COLS_TM_NB)
 #endif
@@ -183,6 +189,9 @@ __host__ __device__ constexpr int fft_ns(int L, int s) { return s == 0 ? 1 : fft
 struct TwTable {
     const float2 *W;
     int S;
+    template <int Ns>
+    __device__ __forceinline__ TwTable pre() const { return *this; }
+    __device__ __forceinline__ void ready() const {}
     template <int Ns, int R>
     __device__ __forceinline__ void get(int, int j, float2 (&w)[8]) const {
         const int k = j % Ns;
@@ -312,20 +321,25 @@ struct Stage {
 
 // stages 1 .. NS-1 with exchanges through `work`; v holds stage-0 outputs on entry
 // and last-stage outputs on exit.  Contains the barriers it needs.
-template <int L, int NB, int STRIDE, int NTH, int SIGN, int s, int NS>
+// TAIL = false drops the barrier after the last stage's loads, for callers whose next
+// write to `work` comes after a barrier of their own.
+template <int L, int NB, int STRIDE, int NTH, int SIGN, int s, int NS, bool TAIL = true>
 struct Mid {
     static constexpr int E = NB * L / NTH;
     template <class TW>
     __device__ static __forceinline__ void run(float2 *work, float2 (&v)[E], int tid, const TW &tw) {
         Stage<L, NB, STRIDE, NTH, s - 1>::store(work, v, tid);
+        // the stage's twiddles (a TMEM provider issues its loads here, under the barrier)
+        auto tws = tw.template pre<Stage<L, NB, STRIDE, NTH, s>::Ns>();
         __syncthreads();
-        Stage<L, NB, STRIDE, NTH, s>::template load_bfly_tw<SIGN>(work, v, tid, tw);
-        __syncthreads();
-        Mid<L, NB, STRIDE, NTH, SIGN, s + 1, NS>::run(work, v, tid, tw);
+        tws.ready();
+        Stage<L, NB, STRIDE, NTH, s>::template load_bfly_tw<SIGN>(work, v, tid, tws);
+        if (TAIL || s + 1 < NS) __syncthreads();
+        Mid<L, NB, STRIDE, NTH, SIGN, s + 1, NS, TAIL>::run(work, v, tid, tw);
     }
 };
-template <int L, int NB, int STRIDE, int NTH, int SIGN, int NS>
-struct Mid<L, NB, STRIDE, NTH, SIGN, NS, NS> {
+template <int L, int NB, int STRIDE, int NTH, int SIGN, int NS, bool TAIL>
+struct Mid<L, NB, STRIDE, NTH, SIGN, NS, NS, TAIL> {
     static constexpr int E = NB * L / NTH;
     template <class TW>
     __device__ static __forceinline__ void run(float2 *, float2 (&)[E], int, const TW &) {}
@@ -344,6 +358,11 @@ struct Fft {
     template <int SIGN, class TW>
     __device__ static __forceinline__ void middle_tw(float2 *work, float2 (&v)[E], int tid, const TW &tw) {
         Mid<L, NB, STRIDE, NTH, SIGN, 1, NS>::run(work, v, tid, tw);
+    }
+    // without the trailing barrier (the caller's next write to `work` follows a barrier)
+    template <int SIGN, class TW>
+    __device__ static __forceinline__ void middle_open(float2 *work, float2 (&v)[E], int tid, const TW &tw) {
+        Mid<L, NB, STRIDE, NTH, SIGN, 1, NS, !COLS_TM_OPEN>::run(work, v, tid, tw);
     }
 };
 
@@ -924,6 +943,26 @@ __global__ void __launch_bounds__(GC<S>::NTH) k_cols(FftArgs A, int mode, const 
 // TMEM columns at base + (slot * 2 + i) * 16, written once per CTA from TwTable (same
 // values), so a transform reads one tcgen05.ld per butterfly instead of 3 shared loads and
 // 4 complex products.
+// Both butterflies' twiddles of one stage, loaded from TMEM ahead of use (TwTmem::pre,
+// before the exchange barrier) and waited for in ready(): the registers pass through the
+// wait so no use can be scheduled above it.
+struct TwRegs {
+    uint32_t r[2][16];
+    __device__ __forceinline__ void ready() {
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+                     : "+r"(r[0][0]), "+r"(r[0][1]), "+r"(r[0][2]), "+r"(r[0][3]), "+r"(r[0][4]), "+r"(r[0][5]),
+                       "+r"(r[0][6]), "+r"(r[0][7]), "+r"(r[0][8]), "+r"(r[0][9]), "+r"(r[0][10]), "+r"(r[0][11]),
+                       "+r"(r[0][12]), "+r"(r[0][13]), "+r"(r[1][0]), "+r"(r[1][1]), "+r"(r[1][2]), "+r"(r[1][3]),
+                       "+r"(r[1][4]), "+r"(r[1][5]), "+r"(r[1][6]), "+r"(r[1][7]), "+r"(r[1][8]), "+r"(r[1][9]),
+                       "+r"(r[1][10]), "+r"(r[1][11]), "+r"(r[1][12]), "+r"(r[1][13])
+                     :: "memory");
+    }
+    template <int Ns, int R>
+    __device__ __forceinline__ void get(int i, int, float2 (&w)[8]) const {
+#pragma unroll
+        for (int k = 1; k < 8; ++k) w[k] = make_float2(__uint_as_float(r[i][2 * k - 2]), __uint_as_float(r[i][2 * k - 1]));
+    }
+};
 struct TwTmem {
     uint32_t base;
     template <int Ns, int R>
@@ -936,6 +975,21 @@ struct TwTmem {
 #pragma unroll
         for (int k = 1; k < 8; ++k) w[k] = make_float2(__uint_as_float(r[2 * k - 2]), __uint_as_float(r[2 * k - 1]));
     }
+#if COLS_TM_TWPRE
+    template <int Ns>
+    __device__ __forceinline__ TwRegs pre() const {
+        static_assert(Ns == 8 || Ns == 64, "512-point radix-8 plan");
+        constexpr int slot = Ns == 8 ? 0 : 1;
+        TwRegs t;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) tm_ld16(base + (uint32_t)((slot * 2 + i) * 16), t.r[i]);
+        return t;
+    }
+#else
+    template <int Ns>
+    __device__ __forceinline__ TwTmem pre() const { return *this; }
+    __device__ __forceinline__ void ready() const {}
+#endif
 };
 
 template <int S>
@@ -1099,7 +1153,7 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
                     S0::template bfly<-1>(&v[i * S0::R], j, Wsm, S);
                     S0::template bfly<-1>(&v[(i + 1) * S0::R], j + 1, Wsm, S);
                 }
-                F::template middle_tw<-1>(work, v, tid, tw);
+                F::template middle_open<-1>(work, v, tid, tw);
                 if (pk) {
 #pragma unroll
                     for (int i = 0; i < SL::BPT; ++i) {
@@ -1168,7 +1222,7 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
             S0::template bfly<+1>(&v[i * S0::R], j, Wsm, S);
         }
         __syncthreads();
-        F::template middle_tw<+1>(work, v, tid, tw);
+        F::template middle_open<+1>(work, v, tid, tw);
         float2 *O = base + (int64_t)A.NQ * S * LDF + f0;
 #pragma unroll
         for (int i = 0; i < SL::BPT; ++i) {
@@ -1197,7 +1251,7 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
             S0::bj(i, tid, t, j);
             S0::template bfly<-1>(&v[i * S0::R], j, Wsm, S);
         }
-        F::template middle_tw<-1>(work, v, tid, tw);
+        F::template middle_open<-1>(work, v, tid, tw);
         tm_put<E>(t_in, v);                        // last-stage positions == stage-0 positions
         tm_wait_st();
         float2 *Bbase = base + (int64_t)S * LDF + f0;
@@ -1227,7 +1281,7 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
                     if (np > td.p1) { np = td.p0; ++nq; }
                     if (nq <= td.q1) prefetch_hhat<S, NB, NTH, LDF>(hbuf, hk(np, nq), f0, tid);
                 }
-                F::template middle_tw<+1>(work, v, tid, tw);
+                F::template middle_open<+1>(work, v, tid, tw);
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     uint32_t a[16];
