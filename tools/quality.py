@@ -1,57 +1,48 @@
 """Deblurring quality of the three methods the paper compares (PAPER.md:266,
 :296-301) on a synthetic star field with a known truth:
 
-  centralized  one facet, Algorithm 1 degenerates to the Local-Solver on Eq. (3)
+  centralized  one facet, no prox term (alpha = 0): the Local-Solver minimises Eq. (3)
   proposed     the facet grid of the config, consensus on the overlaps (Algorithm 1)
   independent  the same facets, no consensus, alpha = 0, omega-blend (deblur independent=1)
+
+Solvers (--solver): vmlmb (default, the paper's setting P:287-290): centralized and
+independent run VMLM-B for --budget inner iterations (the paper: up to 1000), the
+proposed method --outer outer iterations (25) with the 10 + 10k inner schedule;
+pg: every method runs --iters fixed-step projected-gradient steps (the north-star path).
 
 The observation is y = H x_true + n with H the library's own forward operator
 (deblur_apply_H of a one-facet handle: the PSF-interpolation model) and Gaussian
 noise of the config's sigma.  Each method runs the same number of iterations from
-the A6 start; reported: SNR = 10 log10(|x|^2 / |x_hat - x|^2), SSIM (Gaussian
-window 11 / 1.5, data range of x_true), and the global Eq. (3)+TV objective of the
-merged image (evaluated with a one-facet handle).  The paper's qualitative finding
+the A6 start; reported: SNR and SSIM (paper_1705_06603_b200/quality.py, data range of
+x_true), and the global Eq. (3)+TV objective of the merged image (one-facet handle).  The paper's qualitative finding
 is proposed ~ centralized > independent.  GPU only; results -> stdout (JSON lines).
 
-  python tools/quality.py [--config 2] [--n 1024] [--iters 400] [--operator-mode 0]
+  python tools/quality.py [--config 2] [--n 1024] [--solver vmlmb] [--operator-mode 0]
 """
 from __future__ import annotations
 
 import argparse
 import dataclasses
 import json
-import math
 import os
 import sys
 
 import numpy as np
-import scipy.ndimage
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 from paper_1705_06603_b200 import deblur as D  # noqa: E402
-
-
-def snr_db(xh, x):
-    return 10.0 * math.log10(float((x ** 2).sum()) / float(((xh - x) ** 2).sum()))
-
-
-def ssim(a, b, rng_):
-    a = a.astype(np.float64)
-    b = b.astype(np.float64)
-    f = lambda z: scipy.ndimage.gaussian_filter(z, 1.5, truncate=3.5)   # 11-tap window
-    c1, c2 = (0.01 * rng_) ** 2, (0.03 * rng_) ** 2
-    ma, mb = f(a), f(b)
-    va, vb, cab = f(a * a) - ma * ma, f(b * b) - mb * mb, f(a * b) - ma * mb
-    s = ((2 * ma * mb + c1) * (2 * cab + c2)) / ((ma * ma + mb * mb + c1) * (va + vb + c2))
-    return float(s.mean())
+from paper_1705_06603_b200.quality import snr, ssim  # noqa: E402
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--n", type=int, default=None)
-    ap.add_argument("--iters", type=int, default=400)
+    ap.add_argument("--solver", choices=["vmlmb", "pg"], default="vmlmb")
+    ap.add_argument("--iters", type=int, default=400, help="pg: steps of every method")
+    ap.add_argument("--budget", type=int, default=1000, help="vmlmb: centralized / independent inner iterations")
+    ap.add_argument("--outer", type=int, default=25, help="vmlmb: proposed outer iterations (10 + 10k inner)")
     ap.add_argument("--operator-mode", type=int, default=0)
     ap.add_argument("--seed", type=int, default=77)
     args = ap.parse_args()
@@ -67,25 +58,35 @@ def main():
         y_clean = dev.apply_H(x_true)
     rng = np.random.default_rng(args.seed)
     y = (y_clean + sigma * rng.standard_normal(y_clean.shape)).astype(np.float32)
-    methods = {
-        "centralized": dataclasses.replace(one, y=y),
-        "proposed": dataclasses.replace(pb, y=y, independent=0),
-        "independent": dataclasses.replace(pb, y=y, independent=1),
-    }
+    if args.solver == "pg":
+        methods = {
+            "centralized": (dataclasses.replace(one, y=y, independent=1), args.iters),
+            "proposed": (dataclasses.replace(pb, y=y, independent=0), args.iters),
+            "independent": (dataclasses.replace(pb, y=y, independent=1), args.iters),
+        }
+    else:       # VMLM-B; 25 outer iterations of 10 + 10k for the proposed method
+        vm = dict(local_solver=1, inner_increment=0, inner_steps=args.budget)
+        methods = {
+            "centralized": (dataclasses.replace(one, y=y, independent=1, **vm), 1),
+            "proposed": (dataclasses.replace(pb, y=y, independent=0, local_solver=1, inner_steps=10,
+                                             inner_increment=10), args.outer),
+            "independent": (dataclasses.replace(pb, y=y, independent=1, **vm), 1),
+        }
     out = {}
     with D.Deblur.from_problem(dataclasses.replace(one, y=y)) as judge:
-        for name, p in methods.items():
+        for name, (p, iters) in methods.items():
             with D.Deblur.from_problem(p) as dev:
-                dev.iterate(args.iters)
+                dev.iterate(iters)
                 img = dev.get_image()
                 obj_local = dev.objective()
             judge.set_state(img.ravel(), img.ravel())
             tot, data, reg, _ = judge.objective()
-            out[name] = dict(snr_db=round(snr_db(img, x_true), 3), ssim=round(ssim(img, x_true, float(x_true.max() - x_true.min())), 4),
+            out[name] = dict(snr_db=round(snr(x_true, img), 3), ssim=round(ssim(x_true, img, float(x_true.max() - x_true.min())), 4),
                              objective_global=tot, data=data, reg=reg, consensus_maxdiff=obj_local[3],
                              facets=f"{p.fy}x{p.fx}", overlap=p.overlap)
             print(json.dumps({"method": name, **out[name]}), flush=True)
-    print(json.dumps({"config": f"c{args.config}", "n": n, "iters": args.iters, "operator_mode": args.operator_mode,
+    print(json.dumps({"config": f"c{args.config}", "n": n, "solver": args.solver, "iters": args.iters,
+                      "budget": args.budget, "outer": args.outer, "operator_mode": args.operator_mode,
                       "summary": {k: v["snr_db"] for k, v in out.items()}}))
 
 
