@@ -33,7 +33,8 @@ import numpy as np  # noqa: E402
 import synth  # noqa: E402
 
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
-TRAFFIC = os.path.join(ROOT, "profiles", "r1", "traffic.json")     # ncu --set full capture (tools/ncu_full.sh)
+FFMA = os.path.join(ROOT, "profiles", "r2", "ffma_peak.json")      # tools/ffma_peak.cu on a B200 box
+TRAFFIC = os.path.join(ROOT, "profiles", "r2", "traffic.json")     # ncu --set full capture (tools/ncu_full.sh)
 NOMINAL_SMS = 148
 FMA_PER_SM_CLK = 128
 
@@ -151,7 +152,11 @@ def run_ours(args, rank, world, local):
             import torch.distributed as dist
             dist.barrier()
 
+    # warm-up: both start parities of the 2-iteration CUDA graph get captured here, so no
+    # capture / instantiation happens inside the timed region
     dev.iterate(args.warmup)
+    if args.warmup % 2:
+        dev.iterate(3)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = sum(v[0] for k, v in dev.kernel_stats().items() if k != "halo_exchange")
@@ -188,23 +193,38 @@ def run_ours(args, rank, world, local):
     kern = {k: v for k, v in stats.items() if v[0] > 0 and k != "halo_exchange"}
     work = dev.kernel_work()
     pk = peaks()
-    fp32_peak = NOMINAL_SMS * FMA_PER_SM_CLK * 2 * pk.get("sm_max_mhz", 1965.0) / 1e6   # TFLOP/s
+    try:
+        fp32_peak = float(json.load(open(FFMA))["fp32_tflops"])
+        fp32_src = "profiles/r2/ffma_peak.json (measured FFMA, tools/ffma_peak.cu)"
+    except (OSError, ValueError, KeyError):
+        fp32_peak = NOMINAL_SMS * FMA_PER_SM_CLK * 2 * pk.get("sm_max_mhz", 1965.0) / 1e6   # TFLOP/s
+        fp32_src = "fallback: 148 SM x 128 FP32 FMA/clk x 2 x sm_max_mhz (guide unit counts)"
+    ridge = fp32_peak * 1e12 / (pk["hbm_gbs"] * 1e9)          # flop/byte where the two roofs meet
 
     def roof(name):
+        """The kernel's roofline side by its algorithmic intensity (flops / compulsory bytes):
+        above the ridge point the FP32 pipe bounds it (alu), below it HBM does."""
         n, tot_ms = kern[name]
         per = tot_ms / n / 1e3
         fl, by = work.get(name, (0.0, 0.0))
+        alu = fl > 0 and (by <= 0 or fl / by >= ridge)
+        out = {"kernel": name, "ms_per_launch": round(per * 1e3, 4)}
         if fl > 0:
+            out["alu_frac"] = round(fl / per / 1e12 / fp32_peak, 4)
+        if by > 0:
+            out["hbm_frac"] = round(by / per / 1e9 / pk["hbm_gbs"], 4)
+        if by > 0 and fl > 0:
+            out["intensity_flop_per_byte"] = round(fl / by, 2)
+        if alu:
             a = fl / per / 1e12
-            return {"bound": "alu", "achieved": round(a, 3), "peak": round(fp32_peak, 2), "unit": "TFLOP/s",
-                    "frac": round(a / fp32_peak, 4), "traffic": None, "kernel": name,
-                    "ms_per_launch": round(per * 1e3, 4),
-                    "peak_source": "148 SM x 128 FP32 FMA/clk x 2 x sm_max_mhz (guide unit counts)"}
+            out.update({"bound": "alu", "achieved": round(a, 3), "peak": round(fp32_peak, 2), "unit": "TFLOP/s",
+                        "frac": round(a / fp32_peak, 4), "traffic": None, "peak_source": fp32_src})
+            return out
         a = by / per / 1e9 if by > 0 else None
-        return {"bound": "hbm", "achieved": None if a is None else round(a, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": None if a is None else round(a / pk["hbm_gbs"], 4), "traffic": None, "kernel": name,
-                "ms_per_launch": round(per * 1e3, 4),
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "_fallback" not in pk else "fallback"}
+        out.update({"bound": "hbm", "achieved": None if a is None else round(a, 1), "peak": pk["hbm_gbs"],
+                    "unit": "GB/s", "frac": None if a is None else round(a / pk["hbm_gbs"], 4), "traffic": None,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "_fallback" not in pk else "fallback"})
+        return out
 
     dom = max(kern, key=lambda k: kern[k][1])
     roofline = roof(dom)
@@ -222,8 +242,9 @@ def run_ours(args, rank, world, local):
     for k, v in kern.items():
         r = roof(k)
         breakdown[k] = {"launches": v[0], "ms_per_launch": round(v[1] / max(v[0], 1), 4),
-                        "share": round(v[1] / max(tot_ms_all, 1e-9), 4),
-                        "achieved": r["achieved"], "unit": r["unit"], "frac": r["frac"]}
+                        "share": round(v[1] / max(tot_ms_all, 1e-9), 4), "bound": r["bound"],
+                        "achieved": r["achieved"], "unit": r["unit"], "frac": r["frac"],
+                        "hbm_frac": r.get("hbm_frac"), "alu_frac": r.get("alu_frac")}
 
     # end to end through the C ABI with host buffers: reset(y from pinned host) + K iterations + image D2H
     y_pin = torch.from_numpy(pb.y).pin_memory()
@@ -296,6 +317,18 @@ def oracle_sample(pb, n: int):
     return solver.Deblur(pb.psfs, pb.wy[:, o:o + n], pb.wx[:, o:o + n], pb.y[o:o + m, o:o + m], w, 1, 1, 0, prm)
 
 
+def cpu_model() -> str:
+    """lscpu model name of the host (SURVEY §8d asks for it next to the core count)."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(pb, seconds: float):
     n = min(pb.ny, 512)
     d = oracle_sample(pb, n)
@@ -311,6 +344,7 @@ def cpu_baseline(pb, seconds: float):
     dt = time.perf_counter() - t0
     return {"value": round(n2 * n2 * 2 / dt / 1e6, 4), "unit": "Mpixel-iterations/s",
             "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)), "kind": "oracle",
+            "cpu_model": cpu_model(),
             "sample": f"fp64 oracle, 2 iterations on the {n2}x{n2} crop at (N/4, N/4) of c{args_config(pb)} (1 facet)",
             "seconds": round(dt, 2)}
 
@@ -338,7 +372,7 @@ def run_reference(args, rank, world):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded star field, synth/)",
             "config": {"workload": f"c{args.config}", "sample": sample},
             "cpu_baseline": {"value": round(value, 4), "unit": "Mpixel-iterations/s", "cores": cores,
-                             "kind": "oracle", "sample": sample},
+                             "kind": "oracle", "cpu_model": cpu_model(), "sample": sample},
             "e2e": {"value": round(value, 4), "unit": "Mpixel-iterations/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

@@ -233,8 +233,10 @@ DEBLUR_API const char *deblur_kernel_name(int32_t cls);
 DEBLUR_API deblur_status deblur_reset_stats(deblur_t h);
 /* Algorithmic work of ONE launch of kernel class `cls` on this rank (DESIGN.md
  * §5-6): flops = 2 a P^2 per output pixel for the direct stencils (a = number of
- * PSFs with nonzero weight at the pixel), bytes = the compulsory HBM traffic of
- * the pass (FFT passes, elementwise kernels).  0 where not applicable. */
+ * PSFs with nonzero weight at the pixel) and the FFT-convention count of the FFT
+ * passes (5 L log2 L per complex length-L DFT, half that per real one, plus the
+ * spectral products and weights); bytes = the compulsory HBM traffic of the pass
+ * (FFT passes, elementwise kernels).  0 where not applicable. */
 DEBLUR_API deblur_status deblur_kernel_work(deblur_t h, int32_t cls, double *flops, double *bytes);
 
 /* The cudaStream_t (as void*) every kernel of this handle is launched on, so a

@@ -1693,10 +1693,14 @@ deblur_status deblur_kernel_work(deblur_t h, int32_t cls, double *flops, double 
             *flops += 2.0 * P2 * nz_sum(h->h_wy, h->prm.psf_gy, pl.ny, f.ey0, f.ey1) *
                       nz_sum(h->h_wx, h->prm.psf_gx, pl.nx, f.ex0, f.ex1);
     }
-    if (cls >= KC_FFT_H0 && cls <= KC_FFT_HT2 && h->fft)
+    if (cls >= KC_FFT_H0 && cls <= KC_FFT_HT2 && h->fft) {
         *bytes = fft_pass_bytes(*h->fft, cls >= KC_FFT_HT0, (cls - KC_FFT_H0) % 3);
-    if (cls >= KC_FFT2_H0 && cls <= KC_FFT2_HT2 && h->fft2)
+        *flops = fft_pass_flops(*h->fft, cls >= KC_FFT_HT0, (cls - KC_FFT_H0) % 3);
+    }
+    if (cls >= KC_FFT2_H0 && cls <= KC_FFT2_HT2 && h->fft2) {
         *bytes = fft_pass_bytes(*h->fft2, cls >= KC_FFT2_HT0, (cls - KC_FFT2_H0) % 3);
+        *flops = fft_pass_flops(*h->fft2, cls >= KC_FFT2_HT0, (cls - KC_FFT2_H0) % 3);
+    }
     if (cls == KC_UPDATE_G) *bytes = 20.0 * est_px;            // g, u, x in; x+, u|v out
     if (cls == KC_HT_UPDATE) *bytes = 24.0 * est_px;           // r (~obs), x, u in; x+, u|v out
     if (cls == KC_H) *bytes = 4.0 * est_px + 12.0 * obs_px;    // x, y, W in; r out

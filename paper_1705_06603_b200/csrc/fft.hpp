@@ -41,9 +41,15 @@ void fft_destroy(FftPlan *f);
 cudaError_t fft_H_pass(FftPlan &f, int pass, const FacetDev *d_facets, int par, int mode, cudaStream_t s);
 cudaError_t fft_HT_pass(FftPlan &f, int pass, const FacetDev *d_facets, cudaStream_t s);
 // algorithmic HBM bytes moved by one launch of a pass: the pass's
-// compulsory reads/writes of x / r / y / W and of the inter-pass spectra; the PSF
-// spectra (sized to stay L2-resident) are not counted.
+// compulsory reads/writes of x / r / y / W and of the inter-pass spectra.  The PSF
+// spectra are not counted: each Hhat_k (S x (S/2+1) complex, 1.1 MB at S = 512) is shared
+// by the tiles of its PSF cell and re-read per tile; at c4 the 256 spectra (277 MB) do
+// not fit the 126 MB L2, so part of the re-reads reach DRAM (ncu: profiles/).
 double fft_pass_bytes(const FftPlan &f, bool ht, int pass);
+// algorithmic flops of one launch of a pass in the FFT convention:
+// 5 L log2 L per complex length-L DFT, 2.5 L log2 L per real one (R2C / C2R), 6 per
+// complex product, 2 per complex add, 1 per real weight multiply / add.
+double fft_pass_flops(const FftPlan &f, bool ht, int pass);
 int fft_tiles(const FftPlan &f, bool ht);      // tiles of the H (ht = false) or H^T tile list
 
 // per-local-facet data partial sums of the last H pass 2 (after a stream sync).

@@ -1999,6 +1999,25 @@ double fft_pass_bytes(const FftPlan &f, bool ht, int pass) {
     return b;
 }
 
+double fft_pass_flops(const FftPlan &f, bool ht, int pass) {
+    const double S = f.S, T = f.T, NF = f.S / 2 + 1, lg = std::log2((double)f.S);
+    const double cdft = 5.0 * S * lg, rdft = 2.5 * S * lg;   // one length-S transform
+    double fl = 0.0;
+    for (const TileDesc &t : (ht ? f.tHT : f.tH)) {
+        const double nq = std::max(0, t.q1 - t.q0 + 1), npq = nq * std::max(0, t.p1 - t.p0 + 1);
+        if (!ht) {
+            if (pass == 0) fl += nq * S * (S + rdft);                           // x . wx_q, R2C per row
+            else if (pass == 1) fl += NF * (npq * (2.0 * S + cdft + 8.0 * S) + cdft);   // wy_p, DFT, Hhat MAC; inverse
+            else fl += T * rdft + 3.0 * T * T;                                   // C2R rows, W (Hx - y)
+        } else {
+            if (pass == 0) fl += S * rdft;                                       // R2C of the r window rows
+            else if (pass == 1) fl += NF * (cdft + npq * (6.0 * S + cdft + 4.0 * S));  // DFT; conj Hhat, IDFT, wy_p MAC
+            else fl += nq * T * (rdft + 2.0 * S);                                // C2R per q, wx_q MAC
+        }
+    }
+    return fl;
+}
+
 int fft_tiles(const FftPlan &f, bool ht) { return (int)(ht ? f.tHT.size() : f.tH.size()); }
 
 cudaError_t fft_data_partials(FftPlan &f, std::vector<double> &out) {
