@@ -32,46 +32,15 @@
 #include "epilogue.cuh"
 #include "fft.hpp"
 
-#ifndef COLS_TMEM
-#define COLS_TMEM 1
-#endif
-// row passes: a length-S/2 plan over an S table uses W^k, k < S/2, and the R2C / C2R
-// pre/post twiddles W^k, k <= S/2: S/2 + 2 entries (16-byte multiple)
-#ifndef ROWS_TWHALF
-#define ROWS_TWHALF 1
-#endif
-#define ROWS_TW(S) (ROWS_TWHALF ? (S) / 2 + 2 : (S))
-#ifndef COLS_TM_TWHALF
-#define COLS_TM_TWHALF 1
-#endif
-#define COLS_TM_TW (COLS_TM_TWHALF ? S / 2 : S)
-#ifndef COLS_TM_NB
-#define COLS_TM_NB 8
-#endif
-#ifndef COLS_TM_TWTMEM
-#define COLS_TM_TWTMEM 1   // per-thread twiddles of the TMEM column pass in TMEM
-#endif
-#ifndef COLS_TM_CPB
-#define COLS_TM_CPB 3      // column chunks per CTA of the TMEM column pass (when the grid stays >= 4 waves)
-#endif
-#ifndef ROWS_FWD_TMEM
-#define ROWS_FWD_TMEM 1    // R2C pass (H, S = 512): stage-0 inputs stashed in TMEM, xs aliases work
-#endif
-#ifndef ROWS_INV_HT_TMEM
-#define ROWS_INV_HT_TMEM 1 // H^T C2R pass (S = 512): accumulator in TMEM, 3 CTAs/SM
-#endif
-#ifndef COLS_TM_NYQ
-#define COLS_TM_NYQ 1      // TMEM column pass: Nyquist column packed into column 0 (32 chunks, not 33)
-#endif
-#ifndef COLS_TM_OPEN
-#define COLS_TM_OPEN 1     // TMEM column pass: no barrier after a transform's last exchange (callers sync)
-#endif
-#ifndef COLS_TM_TWPRE
-#define COLS_TM_TWPRE 1    // TMEM column pass: a stage's twiddles loaded from TMEM before the exchange barrier
-#endif
-#ifndef COLS_TM_MINB
-#define COLS_TM_MINB (16 / COLS_TM_NB)
-#endif
+// Tuning constants (each measured on c4, B200; alternatives in profiles/r1/SUMMARY.md and
+// profiles/r2/SUMMARY.md).  The row passes keep S/2 + 2 twiddles (a length-S/2 plan over an
+// S table uses W^k, k < S/2, and the R2C / C2R pre/post twiddles W^k, k <= S/2); the TMEM
+// column pass keeps S/2 (a length-S plan uses W^k, k < S/2).
+#define ROWS_TW(S) ((S) / 2 + 2)
+#define COLS_TM_TW (S / 2)
+constexpr int COLS_TM_NB = 8;      // columns per CTA of the TMEM column pass (256 threads, 16 elements each)
+constexpr int COLS_TM_CPB = 3;     // column chunks per CTA (while the grid keeps >= 4 waves of 2 CTAs/SM)
+constexpr int COLS_TM_MINB = 2;    // CTAs per SM (128 registers, ~80 KB smem)
 
 namespace deblur {
 
@@ -362,7 +331,7 @@ struct Fft {
     // without the trailing barrier (the caller's next write to `work` follows a barrier)
     template <int SIGN, class TW>
     __device__ static __forceinline__ void middle_open(float2 *work, float2 (&v)[E], int tid, const TW &tw) {
-        Mid<L, NB, STRIDE, NTH, SIGN, 1, NS, !COLS_TM_OPEN>::run(work, v, tid, tw);
+        Mid<L, NB, STRIDE, NTH, SIGN, 1, NS, false>::run(work, v, tid, tw);
     }
 };
 
@@ -382,7 +351,7 @@ template <int S>
 struct GC {
     // 256 threads, 8 columns per CTA from S = 256 up: ~104 KB smem at S = 512, two CTAs per SM
     static constexpr int NTH = (S <= 128) ? 512 : 256;
-    static constexpr int NB = (S <= 64) ? 64 : (S <= 128) ? 32 : (S == 512 && COLS_TMEM) ? COLS_TM_NB : 8;
+    static constexpr int NB = (S <= 64) ? 64 : (S <= 128) ? 32 : (S == 512) ? COLS_TM_NB : 8;
     static constexpr int CS = S + ((NB >= 16) ? 1 : 16 / NB);
     using F = Fft<S, NB, CS, NTH>;
     static constexpr int E = F::E;
@@ -975,7 +944,6 @@ struct TwTmem {
 #pragma unroll
         for (int k = 1; k < 8; ++k) w[k] = make_float2(__uint_as_float(r[2 * k - 2]), __uint_as_float(r[2 * k - 1]));
     }
-#if COLS_TM_TWPRE
     template <int Ns>
     __device__ __forceinline__ TwRegs pre() const {
         static_assert(Ns == 8 || Ns == 64, "512-point radix-8 plan");
@@ -985,11 +953,6 @@ struct TwTmem {
         for (int i = 0; i < 2; ++i) tm_ld16(base + (uint32_t)((slot * 2 + i) * 16), t.r[i]);
         return t;
     }
-#else
-    template <int Ns>
-    __device__ __forceinline__ TwTmem pre() const { return *this; }
-    __device__ __forceinline__ void ready() const {}
-#endif
 };
 
 template <int S>
@@ -999,14 +962,14 @@ struct GCT {
     static constexpr int NB = COLS_TM_NB, NTH = 32 * NB, CS = S + 16 / NB;
     static constexpr int E = NB * S / NTH;
     // per warp: 32 input + 32 accumulator columns (+ 64 twiddle columns); 4 lane quarters x NB/4 warps
-    static constexpr int WCOLS = COLS_TM_TWTMEM ? 128 : 64;
+    static constexpr int WCOLS = 128;
     static constexpr int TMCOLS = NB >= 8 ? WCOLS * (NB / 4) : WCOLS;
     using F = Fft<S, NB, CS, NTH>;
 };
 template <int S>
 static size_t smem_cols_tm(int NP, int NQ) {
     using G = GCT<S>;
-    return (size_t)COLS_TM_TW * 8 + (size_t)S * G::NB * 8 + (size_t)G::NB * G::CS * 8 + (COLS_TM_NYQ ? 2 * (size_t)S * 8 : 0) +
+    return (size_t)COLS_TM_TW * 8 + (size_t)S * G::NB * 8 + (size_t)G::NB * G::CS * 8 + 2 * (size_t)S * 8 +
            (size_t)NP * S * 4 + (size_t)NP * NQ * 4 + 16;
 }
 
@@ -1024,18 +987,18 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
     float2 *hbuf = Wsm + COLS_TM_TW; // S x NB (prefetched PSF spectrum chunk, pair-interleaved)
     float2 *work = hbuf + S * NB;    // NB x CS
     float2 *hnq = work + NB * CS;    // S: Nyquist column of the PSF spectrum (chunk 0)
-    float2 *nyq = hnq + (COLS_TM_NYQ ? S : 0);   // S: the packed column's spectrum C (chunk 0)
-    float *wys_all = reinterpret_cast<float *>(nyq + (COLS_TM_NYQ ? S : 0));
+    float2 *nyq = hnq + S;           // S: the packed column's spectrum C (chunk 0)
+    float *wys_all = reinterpret_cast<float *>(nyq + S);
     int *slot_s = reinterpret_cast<int *>(wys_all + (size_t)A.NP * S);
     uint32_t *tm_slot = reinterpret_cast<uint32_t *>(slot_s + A.NP * A.NQ);
     const int tid = threadIdx.x, warp = tid >> 5;
     // cpb consecutive column chunks of one tile per CTA: the TMEM allocation,
     // twiddles and the tile's wy_p rows / PSF slots are set up once for all of them
-    // with COLS_TM_NYQ the real columns 0 (DC) and S/2 (Nyquist) of the row spectra travel
+    // for H the real columns 0 (DC) and S/2 (Nyquist) of the row spectra travel
     // as one complex column c = X[., 0] + i X[., S/2] in chunk 0's column 0: S/2 columns
-    static_assert(!COLS_TM_NYQ || (S / 2) % NB == 0, "Nyquist packing needs whole chunks");
+    static_assert((S / 2) % NB == 0, "Nyquist packing needs whole chunks");
     // (H only: for H^T the per-(p, q) combination of the packed column measured slower)
-    const bool nyq_on = COLS_TM_NYQ && mode == 0;
+    const bool nyq_on = mode == 0;
     const int nchunk = nyq_on ? (S / 2) / NB : (NF + NB - 1) / NB;
     const int ngrp = (nchunk + cpb - 1) / cpb;
     const int tile = blockIdx.x / ngrp, cg = blockIdx.x % ngrp;
@@ -1066,7 +1029,6 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
     // this thread's TMEM lane (warp quarter) and its 64 columns: [0, 32) inputs, [32, 64) accumulator
     const uint32_t t_in = *tm_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * G::WCOLS);
     const uint32_t t_acc = t_in + 32;
-#if COLS_TM_TWTMEM
     {
         using S1 = Stage<S, NB, CS, NTH, 1>;
         using S2 = Stage<S, NB, CS, NTH, 2>;
@@ -1091,9 +1053,6 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
         tm_wait_st();
     }
     const TwTmem tw{t_acc + 32};
-#else
-    const TwTable tw{Wsm, S};
-#endif
     const int nqt = td.q1 - td.q0 + 1;
     for (int ci = 0; ci < cpb; ++ci) {
     const int f0 = (cg * cpb + ci) * NB;
@@ -1387,11 +1346,11 @@ struct C2R {
 };
 
 template <int S, bool HT>
-__global__ void __launch_bounds__(256, S == 1024 ? (HT ? 1 : 2) : (HT && S == 512 && ROWS_INV_HT_TMEM) ? 3 : 4)
+__global__ void __launch_bounds__(256, S == 1024 ? (HT ? 1 : 2) : (HT && S == 512) ? 3 : 4)
 k_rows_inv(FftArgs A, int mode) {
     // H^T at S = 512: the accumulator sum_q wx_q C2R(B_q) lives in TMEM (32 columns per
     // thread) instead of 32 registers, so 3 CTAs/SM fit
-    constexpr bool HTT = HT && S == 512 && ROWS_INV_HT_TMEM;
+    constexpr bool HTT = HT && S == 512;
     using G = GR<S>;
     using C = C2R<S>;
     using F = typename G::F;
@@ -1732,13 +1691,11 @@ static cudaError_t setup_attrs(int T, int NP, int NQ) {
     cudaError_t e;
     (void)T;
     if ((e = raise_smem(k_rows_fwd<S, false>, smem_rows_fwd<S>(0, false))) != cudaSuccess) return e;
-    if constexpr (S == 512 && ROWS_FWD_TMEM)
+    if constexpr (S == 512)
         if ((e = raise_smem(k_rows_fwd<S, true>, smem_rows_fwd<S>(0, true))) != cudaSuccess) return e;
     if ((e = raise_smem(k_cols<S>, smem_cols<S>(NP, NQ))) != cudaSuccess) return e;
-#if COLS_TMEM
     if constexpr (S == 512)
         if ((e = raise_smem(k_cols_tm<S>, smem_cols_tm<S>(NP, NQ))) != cudaSuccess) return e;
-#endif
     if ((e = raise_smem(k_rows_inv<S, false>, smem_rows_inv<S>(NQ, false))) != cudaSuccess) return e;
     return raise_smem(k_rows_inv<S, true>, smem_rows_inv<S>(NQ));
 }
@@ -1747,7 +1704,7 @@ template <int S>
 static cudaError_t run_rows_fwd(const FftArgs &a, int ntiles, int mode, int par, const float *psfs, int npsf,
                                 float2 *hrows, cudaStream_t s) {
     if (ntiles == 0) return cudaSuccess;
-    if constexpr (S == 512 && ROWS_FWD_TMEM) {
+    if constexpr (S == 512) {
         if (mode == 0) {
             k_rows_fwd<S, true><<<ntiles * (S / GR<S>::NB), GR<S>::NTH, smem_rows_fwd<S>(mode, true), s>>>(a, mode, par, psfs, npsf, hrows);
             return cudaGetLastError();
@@ -1761,10 +1718,9 @@ static cudaError_t run_cols(const FftArgs &a, int ntiles, int mode, const float2
                             cudaStream_t s) {
     if (ntiles == 0) return cudaSuccess;
     const int nchunk = (S / 2 + 1 + GC<S>::NB - 1) / GC<S>::NB;
-#if COLS_TMEM
     if constexpr (S == 512) {
         if (mode != 2) {
-            const int nck = (COLS_TM_NYQ && mode == 0) ? (S / 2) / GCT<S>::NB : nchunk;
+            const int nck = mode == 0 ? (S / 2) / GCT<S>::NB : nchunk;
             // several chunks per CTA only while the grid keeps >= 4 waves of 2 CTAs per SM
             static const int nsm = [] {       // thread-safe one-time init (one GPU per process)
                 int dev = 0, n = 0;
@@ -1778,7 +1734,6 @@ static cudaError_t run_cols(const FftArgs &a, int ntiles, int mode, const float2
             return cudaGetLastError();
         }
     }
-#endif
     k_cols<S><<<ntiles * nchunk, GC<S>::NTH, smem_cols<S>(a.NP, a.NQ), s>>>(a, mode, hrows, hhat, npsf);
     return cudaGetLastError();
 }

@@ -18,9 +18,7 @@
 namespace deblur {
 namespace {
 
-#ifndef K4_MINB
-#define K4_MINB 4
-#endif
+constexpr int K4_MINB = 4;              // CTAs per SM of K4 (64 registers)
 constexpr int UT_TY = 32, UT_TX = 128;   // update tile (matches the H^T tile grid)
 
 // K4: tile of UT_TY x UT_TX pixels; each thread owns a 4-pixel strip in 4 rows.
@@ -193,12 +191,8 @@ __device__ __forceinline__ float view_at(const View &v, int par, int gy, int gx)
 // y once per CTA (shared memory), so the row loop is loads + arithmetic only.
 // K5_GR rows per load batch, 4 CTAs/SM (61 registers): per-node c4, where almost every pixel
 // is shared by 4 facets, 7.2 -> 5.8 ms against 8 rows at 2 CTAs/SM (profiles/r1/SUMMARY.md)
-#ifndef K5_GR
-#define K5_GR 2            // rows whose loads are in flight together
-#endif
-#ifndef K5_MINB
-#define K5_MINB 4
-#endif
+constexpr int K5_GR = 2;                // rows whose loads are in flight together
+constexpr int K5_MINB = 4;
 __global__ void __launch_bounds__(256, K5_MINB) k_consensus(const FacetDev *facets, const BandRect *rects,
                                                    const RectTile *tiles, int par, float rho) {
     __shared__ float omy_s[2][CT_ROWS];
