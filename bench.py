@@ -127,6 +127,9 @@ def run_ours(args, rank, world, local):
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
+        # the communicator lines (ranks, channels, NVLS / P2P transport) go to stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("gloo")
     pb = synth.make_config(args.config)
     if args.operator_mode == 1:
