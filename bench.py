@@ -145,7 +145,8 @@ def run_ours(args, rank, world, local):
         dist.broadcast(t, 0)
         nid = bytes(t.tolist())
     path = {"direct": D.CONV_DIRECT, "fft": D.CONV_FFT, "auto": D.CONV_AUTO}[args.path]
-    params, keep = D.problem_params(pb, conv_path=path, rank=rank, world=world, device=local, nccl_id_bytes=nid)
+    params, keep = D.problem_params(pb, conv_path=path, rank=rank, world=world, device=local, nccl_id_bytes=nid,
+                                    loopback_world=args.loopback if world == 1 else 0)
     dev = D.Deblur(params, keep)
     stream = torch.cuda.ExternalStream(dev.stream)
 
@@ -293,7 +294,8 @@ def run_ours(args, rank, world, local):
                        "conv_path": {1: "direct", 2: "fft"}[dev.conv_path],
                        "operator_mode": {0: "interpolated H per facet", 1: "per-node PSFs (paper node model)"}[
                            args.operator_mode],
-                       "l2": "no flush: resident state >> 126 MB L2", "parallelism": f"facets over {world} GPU(s)"},
+                       "l2": "no flush: resident state >> 126 MB L2", "parallelism": f"facets over {world} GPU(s)"
+                       + (f", loopback exchange between {args.loopback} virtual ranks" if args.loopback > 1 and world == 1 else "")},
             "gpu_launches": int(launches),
             "roofline": roofline,
             "kernels": breakdown,
@@ -395,6 +397,8 @@ def main():
     ap.add_argument("--inner-inc", type=int, default=0, help="VMLM-B budget increment per outer iteration")
     ap.add_argument("--operator-mode", type=int, choices=[0, 1], default=0,
                     help="0: interpolated H restricted to facets (north star); 1: per-node PSFs, facets = PSF grid")
+    ap.add_argument("--loopback", type=int, default=0,
+                    help="N=1 only: run the multi-rank halo exchange between this many virtual ranks (params.loopback_world)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-crop", type=int, default=1024)

@@ -18,6 +18,8 @@
 //   pass C' : per q C2R along x, weighted by wx_q, summed -> g
 // Every DFT is a radix-8/4/2 Stockham FFT in shared memory with twiddles from a
 // table computed in fp64 on the host and rounded to fp32 (A24).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -611,6 +613,30 @@ __host__ __device__ __forceinline__ int64_t hg_idx(int n, int64_t f, int LDF) { 
 template <int NB>
 __device__ __forceinline__ int hb_idx(int n, int t) { return (((n >> 1) * NB + t) << 1) + (n & 1); }
 
+// mbarrier + TMA (cp.async.bulk.tensor) helpers: one elected thread arms the barrier with
+// the byte count and issues the tensor copy; consumers wait on the barrier's phase parity.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *m, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" :: "r"(smem_u32(m)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *m, uint32_t parity) {
+    asm volatile("{\n .reg .pred p;\n WAIT_%=:\n"
+                 " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                 " @!p bra WAIT_%=;\n}\n" :: "r"(smem_u32(m)), "r"(parity) : "memory");
+}
+// 2-D tiled tensor copy global -> shared, completion counted on mbarrier m (expect_tx armed
+// here by the issuing thread); the generic-proxy reads of dst before it (ordered by the
+// caller's barrier) are fenced against the async-proxy write
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *m,
+                                            uint32_t bytes) {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" :: "r"(smem_u32(m)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+                 :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(m))
+                 : "memory");
+}
+
 // Hhat chunk (S rows x NB columns starting at f0) of spectrum Hk -> smem hbuf with cp.async
 template <int S, int NB, int NTH, int LDF>
 __device__ __forceinline__ void prefetch_hhat(float2 *hbuf, const float2 *Hk, int f0, int tid) {
@@ -969,12 +995,13 @@ struct GCT {
 template <int S>
 static size_t smem_cols_tm(int NP, int NQ) {
     using G = GCT<S>;
-    return (size_t)COLS_TM_TW * 8 + (size_t)S * G::NB * 8 + (size_t)G::NB * G::CS * 8 + 2 * (size_t)S * 8 +
-           (size_t)NP * S * 4 + (size_t)NP * NQ * 4 + 16;
+    return 128 + (size_t)COLS_TM_TW * 8 + (size_t)S * G::NB * 8 + (size_t)G::NB * G::CS * 8 + 2 * (size_t)S * 8 +
+           (size_t)NP * S * 4 + (size_t)NP * NQ * 4 + 16 + 8;
 }
 
 template <int S>
-__global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftArgs A, int mode, int cpb) {
+__global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftArgs A, int mode, int cpb,
+                                                                            const __grid_constant__ CUtensorMap tmh) {
     using G = GCT<S>;
     using F = typename G::F;
     using S0 = typename F::First;
@@ -983,15 +1010,20 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
     constexpr int NB = G::NB, CS = G::CS, E = G::E, LDF = LD<S>::LDF, NF = S / 2 + 1, NTH = G::NTH;
     static_assert(LD<S>::LDF == S / 2 + NB, "chunking shared with k_cols");
     extern __shared__ __align__(16) float2 sm2[];
-    float2 *Wsm = sm2;               // S
-    float2 *hbuf = Wsm + COLS_TM_TW; // S x NB (prefetched PSF spectrum chunk, pair-interleaved)
-    float2 *work = hbuf + S * NB;    // NB x CS
+    // hbuf first, 128-byte aligned: the PSF-spectrum chunk (S x NB, pair-interleaved) lands there
+    // by one TMA tensor copy per (p, q)
+    float2 *hbuf = reinterpret_cast<float2 *>((reinterpret_cast<uintptr_t>(sm2) + 127) & ~static_cast<uintptr_t>(127));
+    float2 *Wsm = hbuf + S * NB;     // S/2 twiddles
+    float2 *work = Wsm + COLS_TM_TW; // NB x CS
     float2 *hnq = work + NB * CS;    // S: Nyquist column of the PSF spectrum (chunk 0)
     float2 *nyq = hnq + S;           // S: the packed column's spectrum C (chunk 0)
     float *wys_all = reinterpret_cast<float *>(nyq + S);
     int *slot_s = reinterpret_cast<int *>(wys_all + (size_t)A.NP * S);
     uint32_t *tm_slot = reinterpret_cast<uint32_t *>(slot_s + A.NP * A.NQ);
+    uint64_t *hbar = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(tm_slot + 1) + 7) & ~static_cast<uintptr_t>(7));
     const int tid = threadIdx.x, warp = tid >> 5;
+    constexpr uint32_t HBYTES = S * NB * 8;
+    uint32_t hphase = 0;
     // cpb consecutive column chunks of one tile per CTA: the TMEM allocation,
     // twiddles and the tile's wy_p rows / PSF slots are set up once for all of them
     // for H the real columns 0 (DC) and S/2 (Nyquist) of the row spectra travel
@@ -1009,6 +1041,10 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
     }
     for (int i = tid; i < COLS_TM_TW; i += NTH) Wsm[i] = A.W[i];   // a length-S forward/inverse plan uses W^k, k < S/2
+    if (tid == 0) {
+        mbar_init(hbar, 1);
+        asm volatile("prefetch.tensormap [%0];\n" :: "l"(reinterpret_cast<uint64_t>(&tmh)) : "memory");
+    }
     const TileDesc td = A.tiles[tile];
     const FacetDev &Fd = A.facets[td.f];
     float2 *base = A.scratch + (int64_t)tile * A.tile_rows * LDF;
@@ -1063,6 +1099,12 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
     // columns 0 and S/2); the inverse DFT of that is real_0 + i real_N
     const bool pk = nyq_on && f0 == 0 && (tid % NB) == 0;
     auto hk = [&](int p, int q) { return A.Hhat + (int64_t)slot_s[(p - td.p0) * nqt + (q - td.q0)] * S * LDF; };
+    // the chunk of PSF spectrum (p, q): pair-rows [slot S/2, +S/2) x floats [4 f0, 4 f0 + 4 NB) of the
+    // 2-D view of Hhat (LDF * 4 floats per pair-row)
+    auto tma_hhat = [&](int p, int q) {
+        if (tid == 0)
+            tma_load_2d(hbuf, &tmh, 4 * f0, slot_s[(p - td.p0) * nqt + (q - td.q0)] * (S / 2), hbar, HBYTES);
+    };
     // stage-0 input positions of this thread, straight from the global chunk (row stride LDF)
     auto load_in = [&](const float2 *src, float2 (&v)[E]) {
 #pragma unroll
@@ -1094,8 +1136,11 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
             tm_wait_st();
             for (int p = td.p0; p <= td.p1; ++p) {
                 __syncthreads();                   // hbuf free
-                if (nyq_on && f0 == 0) prefetch_hnyq<S, NTH, LDF>(hnq, hk(p, q), tid);
-                prefetch_hhat<S, NB, NTH, LDF>(hbuf, hk(p, q), f0, tid);   // under the FFT below
+                if (nyq_on && f0 == 0) {
+                    prefetch_hnyq<S, NTH, LDF>(hnq, hk(p, q), tid);
+                    __pipeline_commit();
+                }
+                tma_hhat(p, q);                    // lands under the FFT below
                 const float *wys = wys_all + (size_t)(p - td.p0) * S;
                 if (p != td.p0) tm_get<E>(t_in, v);
 #pragma unroll
@@ -1122,8 +1167,12 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
                         for (int r = 0; r < SL::R; ++r) nyq[SL::out_n(j, r)] = v[i * SL::R + r];
                     }
                 }
-                __pipeline_wait_prior(0);
-                __syncthreads();                   // Hhat chunk (and nyq) visible
+                mbar_wait(hbar, hphase);           // the TMA of the chunk has landed
+                hphase ^= 1;
+                if (nyq_on && f0 == 0) {           // chunk 0: nyq (other threads' stores) and hnq visible
+                    __pipeline_wait_prior(0);
+                    __syncthreads();
+                }
                 if (pk) {
 #pragma unroll
                     for (int i = 0; i < SL::BPT; ++i) {
@@ -1202,7 +1251,7 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
         }
     } else {
         // mode 1 (H^T): R-hat = DFT_y of the r-window spectrum rows, kept in TMEM
-        if (td.p0 <= td.p1 && td.q0 <= td.q1) prefetch_hhat<S, NB, NTH, LDF>(hbuf, hk(td.p0, td.q0), f0, tid);
+        if (td.p0 <= td.p1 && td.q0 <= td.q1) tma_hhat(td.p0, td.q0);
         load_in(base, v);
 #pragma unroll
         for (int i = 0; i < S0::BPT; ++i) {
@@ -1219,8 +1268,8 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
             for (int p = td.p0; p <= td.p1; ++p) {
                 const float *wys = wys_all + (size_t)(p - td.p0) * S;
                 tm_get<E>(t_in, v);
-                __pipeline_wait_prior(0);
-                __syncthreads();                   // Hhat chunk visible
+                mbar_wait(hbar, hphase);           // Hhat chunk landed (TMA)
+                hphase ^= 1;
 #pragma unroll
                 for (int i = 0; i < S0::BPT; i += 2) {
                     int t, j;
@@ -1238,7 +1287,7 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
                 {
                     int np = p + 1, nq = q;
                     if (np > td.p1) { np = td.p0; ++nq; }
-                    if (nq <= td.q1) prefetch_hhat<S, NB, NTH, LDF>(hbuf, hk(np, nq), f0, tid);
+                    if (nq <= td.q1) tma_hhat(np, nq);
                 }
                 F::template middle_open<+1>(work, v, tid, tw);
 #pragma unroll
@@ -1611,6 +1660,7 @@ struct FftPlan {
     int nlocal = 0;
     const float *wy = nullptr, *wx = nullptr;
     int Ny = 0, Nx = 0;
+    CUtensorMap tmh{};                // TMA view of Hhat for the S = 512 column pass
     std::vector<void *> allocs;
     ~FftPlan() {
         for (void *p : allocs) cudaFree(p);
@@ -1715,7 +1765,7 @@ static cudaError_t run_rows_fwd(const FftArgs &a, int ntiles, int mode, int par,
 }
 template <int S>
 static cudaError_t run_cols(const FftArgs &a, int ntiles, int mode, const float2 *hrows, float2 *hhat, int npsf,
-                            cudaStream_t s) {
+                            const CUtensorMap *tmh, cudaStream_t s) {
     if (ntiles == 0) return cudaSuccess;
     const int nchunk = (S / 2 + 1 + GC<S>::NB - 1) / GC<S>::NB;
     if constexpr (S == 512) {
@@ -1730,7 +1780,8 @@ static cudaError_t run_cols(const FftArgs &a, int ntiles, int mode, const float2
             }();
             int cpb = COLS_TM_CPB;
             while (cpb > 1 && (int64_t)ntiles * ((nck + cpb - 1) / cpb) < 8LL * nsm) --cpb;
-            k_cols_tm<S><<<ntiles * ((nck + cpb - 1) / cpb), GCT<S>::NTH, smem_cols_tm<S>(a.NP, a.NQ), s>>>(a, mode, cpb);
+            k_cols_tm<S><<<ntiles * ((nck + cpb - 1) / cpb), GCT<S>::NTH, smem_cols_tm<S>(a.NP, a.NQ), s>>>(a, mode, cpb,
+                                                                                                      *tmh);
             return cudaGetLastError();
         }
     }
@@ -1764,8 +1815,8 @@ static cudaError_t do_rows_fwd(int S, const FftArgs &a, int nt, int mode, int pa
     return cudaSuccess;
 }
 static cudaError_t do_cols(int S, const FftArgs &a, int nt, int mode, const float2 *hrows, float2 *hhat, int npsf,
-                           cudaStream_t s) {
-    FFT_DISPATCH(S, return run_cols<SS>(a, nt, mode, hrows, hhat, npsf, s));
+                           const CUtensorMap *tmh, cudaStream_t s) {
+    FFT_DISPATCH(S, return run_cols<SS>(a, nt, mode, hrows, hhat, npsf, tmh, s));
     return cudaSuccess;
 }
 static cudaError_t do_rows_inv(int S, const FftArgs &a, int nt, int T, int mode, cudaStream_t s) {
@@ -1907,10 +1958,32 @@ FftPlan *fft_create(const Plan &pl, const std::vector<int> &local, const std::ve
         FftArgs a = f->args(nullptr, false);
         const int n = (int)psf_ids.size();
         FC(do_rows_fwd(S, a, n, 2, 0, d_sel, n, hrows, s));
-        FC(do_cols(S, a, n, 2, hrows, f->Hhat, n, s));
+        FC(do_cols(S, a, n, 2, hrows, f->Hhat, n, nullptr, s));
         FC(cudaStreamSynchronize(s));
         cudaFree(d_sel);
         cudaFree(hrows);
+    }
+    if (S == 512) {
+        // 2-D view of Hhat for the TMEM column pass: rows = pair-rows (nslots * S/2), each
+        // LDF * 4 floats (pair-interleaved complex); box = S/2 pair-rows x 4 NB floats = one
+        // column chunk of one PSF spectrum (32 KB), copied by a single TMA instruction
+        static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+            void *fn = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+                q != cudaDriverEntryPointSuccess)
+                fn = nullptr;
+            return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        }();
+        if (!encode) return fail("cuTensorMapEncodeTiled not available from the driver");
+        const cuuint64_t dims[2] = {(cuuint64_t)LDF * 4, (cuuint64_t)nslots * (S / 2)};
+        const cuuint64_t strides[1] = {(cuuint64_t)LDF * 16};
+        const cuuint32_t box[2] = {(cuuint32_t)(4 * GCT<512>::NB), (cuuint32_t)(S / 2)};
+        const cuuint32_t estr[2] = {1, 1};
+        const CUresult r = encode(&f->tmh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)f->Hhat, dims, strides, box, estr,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail("cuTensorMapEncodeTiled failed for the PSF spectra");
     }
 #undef FC
     return f;
@@ -1922,7 +1995,7 @@ cudaError_t fft_H_pass(FftPlan &f, int pass, const FacetDev *d_facets, int par, 
     FftArgs a = f.args(d_facets, false);
     const int n = (int)f.tH.size();
     if (pass == 0) return do_rows_fwd(f.S, a, n, 0, par, nullptr, 0, nullptr, s);
-    if (pass == 1) return do_cols(f.S, a, n, 0, nullptr, nullptr, 0, s);
+    if (pass == 1) return do_cols(f.S, a, n, 0, nullptr, nullptr, 0, &f.tmh, s);
     return do_rows_inv(f.S, a, n, f.T, mode, s);
 }
 
@@ -1930,7 +2003,7 @@ cudaError_t fft_HT_pass(FftPlan &f, int pass, const FacetDev *d_facets, cudaStre
     FftArgs a = f.args(d_facets, true);
     const int n = (int)f.tHT.size();
     if (pass == 0) return do_rows_fwd(f.S, a, n, 1, 0, nullptr, 0, nullptr, s);
-    if (pass == 1) return do_cols(f.S, a, n, 1, nullptr, nullptr, 0, s);
+    if (pass == 1) return do_cols(f.S, a, n, 1, nullptr, nullptr, 0, &f.tmh, s);
     return do_rows_inv(f.S, a, n, f.T, INV_HT, s);
 }
 
