@@ -104,3 +104,19 @@ def test_full_size_against_golden(name):
             assert abs(tr[it, i] - trace_ref[it, i]) <= OBJ_TOL * abs(trace_ref[it, i]), (it, i, tr[it, i])
         assert abs(tr[it, 3] - trace_ref[it, 3]) <= IT_TOL * max(1.0, np.abs(g["x"]).max())
     assert trace_ref[iters, 0] < trace_ref[0, 0]             # the run makes progress
+
+
+def test_c5_objective_at_start_against_golden():
+    """c5 (32768^2, 32x32 PSFs of 127^2, 8x8 facets) at full size: Eq. (4) at the A6 start
+    against the oracle's facet-by-facet evaluation (tools/make_golden.py --objective-only;
+    a full c5 oracle iteration does not fit the host's memory, the iterate at c5 is checked
+    at sampled interior and band pixels in test_gpu_fullsize.py)."""
+    g = load("c5_obj0")
+    pb = synth.make_config(5)
+    assert synth.input_hash(pb) == str(g["input_hash"])
+    with D.Deblur.from_problem(pb) as dev:
+        obj = dev.objective()
+    ref = g["trace"][0]
+    for i in range(3):
+        assert abs(obj[i] - ref[i]) <= OBJ_TOL * abs(ref[i]), (i, obj[i], ref[i])
+    assert obj[3] == 0.0                                     # every facet starts from the same x0

@@ -17,6 +17,9 @@ geometry and stores
 
 Usage:  python tools/make_golden.py 3 100      (c3, 100 iterations: ~2 h on 8 cores)
         python tools/make_golden.py 4 2        (c4, a stated 2-iteration prefix)
+        python tools/make_golden.py 5 0 --objective-only
+                                               (c5: Eq. (4) at the A6 start, facet by facet; a full
+                                                c5 oracle iteration needs > 62 GB of host memory)
 """
 from __future__ import annotations
 
@@ -75,6 +78,39 @@ def sample_state(facets, rng, n_random, n_per_class):
     return idx.astype(np.int64)
 
 
+def objective_only(a):
+    """Eq. (4) (A22) at x^(0) = u^(0) = the A6 start, per facet with the oracle's own
+    pieces: data_f = 1/2 sum_{O_f} W (H_f x_f - y)^2 (Operator.H_window), reg_f = sum phi(D x_f)
+    (tv.value, circular per facet); the facets agree at the start, so the consensus
+    max-difference is 0."""
+    from oracle import Operator, tv
+    t0 = time.time()
+    pb = synth.make_config(a.k)
+    h = synth.input_hash(pb)
+    facets = geometry.plan(pb.ny, pb.nx, pb.P, pb.fy, pb.fx, pb.overlap)
+    op = Operator(pb.psfs, pb.wy, pb.wx)
+    c = op.c
+    y = pb.y
+    w_s = np.float64(np.float32(pb.noise_w_scalar))
+    data = np.zeros(len(facets))
+    reg = np.zeros(len(facets))
+    for i, f in enumerate(facets):
+        # x0 restricted to P_f: max(0, y edge-replicated into the c-wide margin) (A6)
+        rows = np.clip(np.arange(f.ey[0], f.ey[1]) - c, 0, pb.my - 1)
+        cols = np.clip(np.arange(f.ex[0], f.ex[1]) - c, 0, pb.mx - 1)
+        xf = np.maximum(0.0, y[np.ix_(rows, cols)].astype(np.float64))
+        d = op.H_window(xf, f.ey[0], f.ex[0]) - y[f.oy[0]:f.oy[1], f.ox[0]:f.ox[1]].astype(np.float64)
+        w = pb.noise_w[f.oy[0]:f.oy[1], f.ox[0]:f.ox[1]].astype(np.float64) if pb.noise_w is not None else w_s
+        data[i] = 0.5 * float((w * d * d).sum())
+        reg[i] = tv.value(xf, pb.eps, pb.reg_kind, pb.tv_boundary)
+        print(f"  facet {i}: data {data[i]:.9e} reg {reg[i]:.9e} ({time.time() - t0:.0f} s)", flush=True)
+    tot_d, tot_r = float(data.sum()), float(pb.lam * reg.sum())
+    out = a.out or os.path.join(GOLDEN, f"c{a.k}_obj0.npz")
+    np.savez_compressed(out, config=a.k, iters=0, input_hash=h, trace=np.array([[tot_d + tot_r, tot_d, tot_r, 0.0]]),
+                        made_by="tools/make_golden.py --objective-only (oracle/ + synth/ only)")
+    print(f"wrote {out}: objective {tot_d + tot_r:.12e} ({time.time() - t0:.0f} s)", flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("k", type=int)
@@ -82,7 +118,11 @@ def main():
     ap.add_argument("--n-random", type=int, default=60000)
     ap.add_argument("--n-class", type=int, default=20000)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--objective-only", action="store_true",
+                    help="only Eq. (4) at the A6 start, evaluated facet by facet (no global arrays)")
     a = ap.parse_args()
+    if a.objective_only:
+        return objective_only(a)
 
     t0 = time.time()
     pb = synth.make_config(a.k)
