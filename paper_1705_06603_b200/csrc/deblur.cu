@@ -110,7 +110,8 @@ struct deblur_ctx {
     int64_t stat_n[KC_COUNT] = {0};
     double stat_ms[KC_COUNT] = {0};
     // persistent staging buffers for reset / get_image (allocated on first use)
-    float *d_ystage = nullptr;
+    float *d_ystage = nullptr;            // staged observed image (bounding box of this rank's needs)
+    int64_t ys_y0 = 0, ys_x0 = 0, ys_pitch = 1;
     float *d_image = nullptr;
     // CUDA graphs of two full iterations (parity returns to its start), one per start parity
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
@@ -352,12 +353,43 @@ static deblur_status upload_slice(deblur_t h, float *dst, int64_t dpitch, const 
     return DEBLUR_OK;
 }
 
-// x0 given: upload its facet slices to x[0] and copy to u.  x0 == NULL: the A6
-// default computed on the device from the observed rows/cols each facet needs.
-static deblur_status upload_state_x0(deblur_t h, const float *x0, const float *y) {
+// The observed image crosses PCIe once: the bounding box of what this rank's facets need
+// (their observed blocks O_f for y, and O_f dilated by c -- clipped -- for the A6 start)
+// is uploaded into a staging buffer; F.y and the A6 start are formed from it on the device.
+static deblur_status stage_y(deblur_t h, const float *y) {
     const Plan &pl = h->plan;
     const int c = (pl.P - 1) / 2;
-    float *ydil = nullptr;
+    int64_t y0 = pl.my, y1 = 0, x0 = pl.mx, x1 = 0;
+    for (int id : h->local) {
+        const FacetPlan &fp = pl.facets[id];
+        y0 = std::min(y0, std::max<int64_t>(0, fp.ey0 - c)); y1 = std::max(y1, std::min<int64_t>(pl.my, fp.ey1 - c));
+        x0 = std::min(x0, std::max<int64_t>(0, fp.ex0 - c)); x1 = std::max(x1, std::min<int64_t>(pl.mx, fp.ex1 - c));
+    }
+    if (!h->d_ystage) CU(h->dalloc(&h->d_ystage, (size_t)pl.my * pl.mx));
+    h->ys_y0 = y0; h->ys_x0 = x0; h->ys_pitch = std::max<int64_t>(1, x1 - x0);
+    if (y1 > y0 && x1 > x0)
+        CU(cudaMemcpy2DAsync(h->d_ystage, h->ys_pitch * 4, y + y0 * pl.mx + x0, pl.mx * 4, (x1 - x0) * 4, y1 - y0,
+                             cudaMemcpyHostToDevice, h->stream));
+    return DEBLUR_OK;
+}
+
+// F.y of every local facet from the staged y (device copies)
+static deblur_status upload_y(deblur_t h) {
+    for (size_t li = 0; li < h->local.size(); ++li) {
+        const FacetPlan &fp = h->plan.facets[h->local[li]];
+        FacetDev &F = h->fh[li];
+        const float *src = h->d_ystage + (fp.oy0 - h->ys_y0) * h->ys_pitch + (fp.ox0 - h->ys_x0);
+        CU(cudaMemcpy2DAsync((float *)F.y, F.op * 4, src, h->ys_pitch * 4, F.mx * 4, F.my, cudaMemcpyDeviceToDevice,
+                             h->stream));
+    }
+    return DEBLUR_OK;
+}
+
+// x0 given: upload its facet slices to x[0] and copy to u.  x0 == NULL: the A6
+// default computed on the device from the staged y.
+static deblur_status upload_state_x0(deblur_t h, const float *x0) {
+    const Plan &pl = h->plan;
+    const int c = (pl.P - 1) / 2;
     for (size_t li = 0; li < h->local.size(); ++li) {
         const FacetPlan &fp = pl.facets[h->local[li]];
         FacetDev &F = h->fh[li];
@@ -366,28 +398,12 @@ static deblur_status upload_state_x0(deblur_t h, const float *x0, const float *y
             if (s != DEBLUR_OK) return s;
             CU(cudaMemcpy2DAsync(F.u, F.ep * 4, F.x[0], F.ep * 4, F.nx * 4, F.ny, cudaMemcpyDeviceToDevice, h->stream));
         } else {
-            const int64_t y0 = std::max<int64_t>(0, fp.ey0 - c), y1 = std::min<int64_t>(pl.my, fp.ey1 - c);
-            const int64_t x0c = std::max<int64_t>(0, fp.ex0 - c), x1 = std::min<int64_t>(pl.mx, fp.ex1 - c);
-            const int64_t w = x1 - x0c, hh = y1 - y0;
-            if (!h->d_ystage) CU(h->dalloc(&h->d_ystage, (size_t)(pl.my + 2) * (pl.mx + 2)));
-            ydil = h->d_ystage;
-            CU(cudaMemcpy2DAsync(ydil, w * 4, y + y0 * pl.mx + x0c, pl.mx * 4, w * 4, hh, cudaMemcpyHostToDevice,
-                                 h->stream));
-            CU(launch_x0_from_y(F, ydil, w, (int)y0, (int)x0c, (int)pl.my, (int)pl.mx, c, h->stream));
+            CU(launch_x0_from_y(F, h->d_ystage, h->ys_pitch, (int)h->ys_y0, (int)h->ys_x0, (int)pl.my, (int)pl.mx, c,
+                                h->stream));
         }
     }
     h->par = 0;
     CU(cudaStreamSynchronize(h->stream));
-    return DEBLUR_OK;
-}
-
-static deblur_status upload_y(deblur_t h, const float *y) {
-    for (size_t li = 0; li < h->local.size(); ++li) {
-        const FacetPlan &fp = h->plan.facets[h->local[li]];
-        FacetDev &F = h->fh[li];
-        deblur_status s = upload_slice(h, (float *)F.y, F.op, y, h->plan.mx, fp.oy0, fp.ox0, F.my, F.mx);
-        if (s != DEBLUR_OK) return s;
-    }
     return DEBLUR_OK;
 }
 
@@ -885,9 +901,10 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
     h->sc.tau = (float)h->tau; h->sc.reg_kind = p->reg_kind; h->sc.tv_boundary = p->tv_boundary;
 
     // data + initial state
-    st = upload_y(h, p->y);
+    st = stage_y(h, p->y);
+    if (st == DEBLUR_OK) st = upload_y(h);
     if (st != DEBLUR_OK) { g_last_error = h->err; return st; }
-    st = upload_state_x0(h, p->x0, p->y);
+    st = upload_state_x0(h, p->x0);
     if (st != DEBLUR_OK) { g_last_error = h->err; return st; }
 
     // FFT path plan
@@ -1604,9 +1621,10 @@ deblur_status deblur_reset(deblur_t h, const float *y, const float *x0) {
     deblur_status s = check_state(h);
     if (s != DEBLUR_OK) return s;
     if (!y) return h->fail(DEBLUR_EINVAL, "y is NULL");
-    if ((s = upload_y(h, y)) != DEBLUR_OK) return s;
+    if ((s = stage_y(h, y)) != DEBLUR_OK) return s;
+    if ((s = upload_y(h)) != DEBLUR_OK) return s;
     h->vm.k_outer = 0;                                // a fresh solve: VMLM-B budget schedule restarts
-    return upload_state_x0(h, x0, y);
+    return upload_state_x0(h, x0);
 }
 
 deblur_status deblur_get_outer_iteration(deblur_t h, int32_t *k) {
