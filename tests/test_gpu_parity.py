@@ -491,3 +491,27 @@ def test_vmlmb_reset_restarts_the_budget_schedule():
         xb, ub = dev.get_state()
     np.testing.assert_array_equal(xa, xb)
     np.testing.assert_array_equal(ua, ub)
+
+
+def test_vmlmb_checkpoint_resume_with_outer_iteration():
+    """A checkpoint of (x_f, u_f, k) resumes the VMLM-B run exactly: the inner budget
+    inner_steps + k inner_increment continues from the stored outer iteration k."""
+    pb = synth.make_config(2, n=200, facets=(2, 2), overlap=20)
+    pb.local_solver, pb.inner_steps, pb.inner_increment = 1, 4, 3
+    with D.Deblur.from_problem(pb, conv_path=D.CONV_FFT) as dev:
+        dev.iterate(3)
+        xa, ua = dev.get_state()
+    with D.Deblur.from_problem(pb, conv_path=D.CONV_FFT) as dev:
+        dev.iterate(2)
+        xs, us = dev.get_state()
+        k = dev.outer_iteration
+    assert k == 2
+    with D.Deblur.from_problem(pb, conv_path=D.CONV_FFT) as dev:
+        dev.set_state(xs, us)
+        dev.outer_iteration = k
+        dev.iterate(1)
+        xb, ub = dev.get_state()
+        with pytest.raises(ValueError):
+            dev.set_state(xs[:-1], us)
+    np.testing.assert_array_equal(xa, xb)
+    np.testing.assert_array_equal(ua, ub)
