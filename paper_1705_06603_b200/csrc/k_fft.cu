@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <tuple>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -43,6 +44,7 @@
 constexpr int COLS_TM_NB = 8;      // columns per CTA of the TMEM column pass (256 threads, 16 elements each)
 constexpr int COLS_TM_CPB = 3;     // column chunks per CTA (while the grid keeps >= 4 waves of 2 CTAs/SM)
 constexpr int COLS_TM_MINB = 2;    // CTAs per SM (128 registers, ~80 KB smem)
+
 
 namespace deblur {
 
@@ -1905,6 +1907,20 @@ FftPlan *fft_create(const Plan &pl, const std::vector<int> &local, const std::ve
                     if (t.q1 < t.q0) { t.q0 = 0; t.q1 = -1; }
                     f->tHT.push_back(t);
                 }
+    }
+    // PSF-cell-major tile order: tiles with the same active PSF range run back to back, so
+    // the CTAs in flight share their PSF spectra in L2
+    {
+        std::vector<int> ord(f->tH.size());
+        for (size_t i = 0; i < ord.size(); ++i) ord[i] = (int)i;
+        auto key = [](const TileDesc &t) { return std::make_tuple(t.p0, t.q0, t.p1, t.q1); };
+        std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return key(f->tH[a]) < key(f->tH[b]); });
+        std::vector<TileDesc> th;
+        std::vector<int> tf;
+        for (int i : ord) { th.push_back(f->tH[i]); tf.push_back(f->tile_facet_H[i]); }
+        f->tH.swap(th);
+        f->tile_facet_H.swap(tf);
+        std::stable_sort(f->tHT.begin(), f->tHT.end(), [&](const TileDesc &a, const TileDesc &b) { return key(a) < key(b); });
     }
     for (auto *lst : {&f->tH, &f->tHT})
         for (auto &t : *lst) {
