@@ -11,6 +11,10 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 bash tools/ncu_full.sh ${TAG}
 python tools/traffic_from_ncu.py gpurun_out/${TAG}.ncu-rep gpurun_out/${TAG}_traffic.json > /dev/null 2>&1; echo "traffic rc=$?"
 [ -n "$QUICK" ] && exit 0
+for k in 1 2 3; do
+  timeout 600 python bench.py --config $k --steps 40 --no-cpu > gpurun_out/${TAG}_c$k.json 2> gpurun_out/${TAG}_c$k.err; tail -c 200 gpurun_out/${TAG}_c$k.json
+done
+timeout 600 python bench.py --loopback 8 --no-cpu > gpurun_out/${TAG}_c4_loop8.json 2> gpurun_out/${TAG}_c4_loop8.err; tail -c 200 gpurun_out/${TAG}_c4_loop8.json
 timeout 600 python bench.py --config 5 --steps 3 --no-cpu > gpurun_out/${TAG}_c5.json 2> gpurun_out/${TAG}_c5.err; tail -c 300 gpurun_out/${TAG}_c5.json
 timeout 600 python bench.py --operator-mode 1 --no-cpu > gpurun_out/${TAG}_c4_pernode.json 2> gpurun_out/${TAG}_c4_pernode.err; tail -c 300 gpurun_out/${TAG}_c4_pernode.json
 timeout 900 python bench.py --config 6 --steps 3 --no-cpu > gpurun_out/${TAG}_c6.json 2> gpurun_out/${TAG}_c6.err; tail -c 300 gpurun_out/${TAG}_c6.json
