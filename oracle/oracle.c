@@ -19,12 +19,25 @@
  * evaluated at GLOBAL coordinates.
  *
  * Loop order is row-axpy (SURVEY §8d "loop order matters"): the same sum,
- * terms skipped only where omega_k == 0 exactly.  OpenMP over output rows.
+ * terms skipped only where omega_k == 0 exactly (rows where wy_p = 0, and columns
+ * outside the support [tlo, thi] of wx_q on the window: the skipped terms are exact
+ * zeros, so every nonzero term is added in the same order).  OpenMP over output rows.
  */
+
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+
+/* [*lo, *hi] = first / last index of w[0..n) that is nonzero (lo > hi: none) */
+static void nz_span(const double *w, int64_t n, int64_t *lo, int64_t *hi)
+{
+    *lo = 0; *hi = -1;
+    while (*lo < n && w[*lo] == 0.0) ++*lo;
+    if (*lo == n) return;
+    *hi = n - 1;
+    while (w[*hi] == 0.0) --*hi;
+}
 
 /* out[(ny-P+1) x (nx-P+1)] = H_f x_win.  x_win is [ny][nx] at global origin (e0y, e0x). */
 void orc_H_window(int64_t Ny, int64_t Nx, int P, int Gy, int Gx,
@@ -47,6 +60,8 @@ void orc_H_window(int64_t Ny, int64_t Nx, int P, int Gy, int Gx,
             int anyx = 0;
             for (int64_t t = 0; t < nx && !anyx; ++t) anyx = (wxq[t] != 0.0);
             if (!any || !anyx) continue;
+            int64_t tlo, thi;                     /* columns of the window where wx_q != 0 */
+            nz_span(wxq, nx, &tlo, &thi);
             /* W_k C_k x : weighted copy of the window */
             #pragma omp parallel for schedule(static)
             for (int64_t r = 0; r < ny; ++r)
@@ -64,7 +79,11 @@ void orc_H_window(int64_t Ny, int64_t Nx, int P, int Gy, int Gx,
                     for (int b = 0; b < P; ++b) {
                         const double hv = h[a * P + b];
                         const double *src = row + (c2 - b);
-                        for (int64_t j = 0; j < mx; ++j) o[j] += hv * src[j];
+                        /* src[j] = xw[li][j + c2 - b] is zero unless tlo <= j + c2 - b <= thi */
+                        int64_t j0 = tlo - c2 + b, j1 = thi - c2 + b + 1;
+                        if (j0 < 0) j0 = 0;
+                        if (j1 > mx) j1 = mx;
+                        for (int64_t j = j0; j < j1; ++j) o[j] += hv * src[j];
                     }
                 }
             }
@@ -89,6 +108,9 @@ void orc_HT_window(int64_t Ny, int64_t Nx, int P, int Gy, int Gx,
             const double *wyp = wy + (int64_t)p * Ny + e0y;
             const double *wxq = wx + (int64_t)q * Nx + e0x;
             const double *h = psfs + (int64_t)(p * Gx + q) * P * P;
+            int64_t tlo, thi;                     /* columns of the window where wx_q != 0 */
+            nz_span(wxq, nx, &tlo, &thi);
+            if (tlo > thi) continue;
             #pragma omp parallel
             {
                 double *corr = (double *)malloc(sizeof(double) * (size_t)nx);
@@ -104,14 +126,14 @@ void orc_HT_window(int64_t Ny, int64_t Nx, int P, int Gy, int Gx,
                             const double hv = h[a * P + b];
                             /* corr[q] += h[a][b] * r[ri][q - 2c + b] for valid columns */
                             int64_t q0 = c2 - b, q1 = mx + c2 - b; /* q in [q0, q1) */
-                            if (q0 < 0) q0 = 0;
-                            if (q1 > nx) q1 = nx;
+                            if (q0 < tlo) q0 = tlo;           /* corr is used only where wx_q != 0 */
+                            if (q1 > thi + 1) q1 = thi + 1;
                             const double *src = rrow + (b - c2);
                             for (int64_t qq = q0; qq < q1; ++qq) corr[qq] += hv * src[qq];
                         }
                     }
                     double *go = g + pr * nx;
-                    for (int64_t qq = 0; qq < nx; ++qq) go[qq] += wyp[pr] * wxq[qq] * corr[qq];
+                    for (int64_t qq = tlo; qq <= thi; ++qq) go[qq] += wyp[pr] * wxq[qq] * corr[qq];
                 }
                 free(corr);
             }
