@@ -130,6 +130,41 @@ __device__ __forceinline__ float update_value_t(int ny, int nx, const float *xh,
     return xn;
 }
 
+// TV gradient of 4 adjacent pixels (i, j .. j+3) of one row, smoothed TV with the circular D
+// (the path of the north-star step): psi_x(q - 1) of pixel q is psi(q - 1) of its left
+// neighbour in the strip, so the strip needs psi at (i, j-1 .. j+3) and (i-1, j .. j+3):
+// 9 reciprocal square roots instead of 12, each with the same operands as tv_grad_t's.
+__device__ __forceinline__ void tv_grad4(const float *xh, int XH, int i, int j, const SolverConst &sc,
+                                         bool want_phi, float (&td)[4], float (&phi)[4]) {
+    const float e2 = sc.eps * sc.eps;
+    const float *r0 = xh + (i - 1) * XH + j, *r1 = xh + i * XH + j, *r2 = xh + (i + 1) * XH + j;
+    float a[5], b[6], c[5];                        // rows i-1 (j..j+4), i (j-1..j+4), i+1 (j-1..j+3)
+#pragma unroll
+    for (int k = 0; k < 5; ++k) { a[k] = r0[k]; c[k] = r2[k - 1]; }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) b[k] = r1[k - 1];
+    float dy[5], dx[5], s[5];                      // psi at (i, j-1+k): D and 1/sqrt(|D|^2 + eps^2)
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        dy[k] = c[k] - b[k];
+        dx[k] = b[k + 1] - b[k];
+        s[k] = rsqrtf(dy[k] * dy[k] + dx[k] * dx[k] + e2);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const float xc = b[q + 1];
+        const float dyu = xc - a[q], dxu = a[q + 1] - a[q];      // psi at (i-1, j+q)
+        const float su = rsqrtf(dyu * dyu + dxu * dxu + e2);
+        // psi_y(p-1) - psi_y(p) + psi_x(q-1) - psi_x(q)
+        td[q] = dyu * su - dy[q + 1] * s[q + 1] + dx[q] * s[q] - dx[q + 1] * s[q + 1];
+        phi[q] = 0.f;
+        if (want_phi) {
+            const float t2c = dy[q + 1] * dy[q + 1] + dx[q + 1] * dx[q + 1];
+            phi[q] = t2c / (sqrtf(t2c + e2) + sc.eps);
+        }
+    }
+}
+
 // stage the (TYh+2) x (TXh+2) circular halo of x[par] for a tile at (y0, x0)
 __device__ __forceinline__ void stage_halo(const FacetDev &F, float *xh, int XH, int YH, int y0, int x0, int par) {
     const float *__restrict__ x = F.x[par];

@@ -114,6 +114,21 @@ __global__ void __launch_bounds__(EPI_NT, K4_MINB) k_update_from_g(const FacetDe
         const bool shxj[4] = {shx.x != 0, shx.y != 0, shx.z != 0, shx.w != 0};
         float xn[4], nu[4], nv[4];
         bool sh[4];
+        if constexpr (REG == 0 && !NEU) {
+            // the strip's TV gradient with shared psi evaluations (tv_grad4)
+            float td[4], ph[4];
+            tv_grad4(xh, XH, ly + 1, lx0 + 4, sc, partials != nullptr, td, ph);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                sh[j] = shy || shxj[j];
+                const float xc = xh[(ly + 1) * XH + lx0 + 4 + j];
+                const float gt = gv[k][j] + sc.lambda * td[j] + sc.gamma * (omy * omxj[j]) * (xc - uv[k][j]);
+                xn[j] = fmaxf(0.f, xc - sc.tau * gt);
+                nu[j] = uv[k][j] + sc.rho * (xn[j] - uv[k][j]);
+                nv[j] = 2.f * xn[j] - uv[k][j];
+                if (fx0 + j < F.nx) rsum += (double)ph[j];
+            }
+        } else {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int fx = fx0 + j;
@@ -122,6 +137,7 @@ __global__ void __launch_bounds__(EPI_NT, K4_MINB) k_update_from_g(const FacetDe
             xn[j] = update_value_t<REG, NEU>(F.ny, F.nx, xh, XH, ly + 1, lx0 + j + 4, fy, fx, gv[k][j], uv[k][j],
                                              omy * omxj[j], sc, partials != nullptr, phi, nu[j], nv[j]);
             if (fx < F.nx) rsum += (double)phi;
+        }
         }
         if (full) {
             *reinterpret_cast<float4 *>(xo + o) = make_float4(xn[0], xn[1], xn[2], xn[3]);
