@@ -570,7 +570,9 @@ __global__ void __launch_bounds__(256, S == 512 ? 4 : S == 1024 ? 2 : 5) k_rows_
             }
             S0::template bfly<-1>(&v[i * S0::R], j, Wsm, S);
         }
-        __syncthreads();      // Wsm/xs readers done before work is written (work is disjoint; keeps phases clean)
+        // stage 0 read xs, which aliases work at S = 512 outside the TMEM-stash variant: its
+        // readers finish before middle() writes work (elsewhere stage 0 reads TMEM / a disjoint xs)
+        if (S == 512 && !tmx) __syncthreads();
         F::template middle<-1>(work, v, tid, Wsm, S);
         F::Last::store(work, v, tid);
         __syncthreads();
