@@ -81,3 +81,19 @@ def test_loopback_matches_oracle():
     xr, ur = orc.state()
     assert np.linalg.norm(xs - xr) / np.linalg.norm(xr) <= 1e-3
     assert np.linalg.norm(us - ur) / np.linalg.norm(ur) <= 1e-3
+
+
+@pytest.mark.parametrize("V", [4, 16])
+def test_loopback_per_node_and_independent(V):
+    """Per-node operators (16 facets = the 4x4 PSF grid, nearly every pixel shared by 4
+    facets) and the independent baseline (no exchange at all) over the loopback transport."""
+    base = synth.per_node(synth.make_config(2, n=300))
+    for pb in (base, synth.make_config(2, n=300, facets=(4, 4), overlap=20)):
+        if pb is not base:
+            pb.independent = 1
+        x1, u1, o1, i1, _ = run(pb, 4, 0, D.CONV_FFT)
+        xv, uv, ov, iv, _ = run(pb, 4, V, D.CONV_FFT)
+        np.testing.assert_array_equal(xv, x1)
+        np.testing.assert_array_equal(uv, u1)
+        np.testing.assert_array_equal(ov, o1)
+        np.testing.assert_array_equal(iv, i1)
