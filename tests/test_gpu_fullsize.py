@@ -24,6 +24,7 @@ import numpy as np
 import pytest
 
 import synth
+from tests.fullsize import full_config
 from oracle import Operator, geometry, solver, tv
 from paper_1705_06603_b200 import deblur as D
 
@@ -89,7 +90,7 @@ def _oracle_update(pb, op, X, U, tau, gy, gx):
 
 @pytest.mark.parametrize("k,count", [(4, 24), (5, 12)], ids=["c4", "c5"])
 def test_iterate_full_size_sampled(k, count):
-    pb = synth.make_config(k)
+    pb = full_config(k)
     facets = geometry.plan(pb.ny, pb.nx, pb.P, pb.fy, pb.fx, pb.overlap)
     w_max = float(pb.noise_w.max()) if pb.noise_w is not None else float(np.float32(pb.noise_w_scalar))
     tau = solver.default_tau(pb.psfs, pb.wy, pb.wx, w_max, pb.lam, pb.eps, pb.reg_kind, pb.gamma)
@@ -187,7 +188,7 @@ def test_iterate_full_size_band_pixels(k, count):
     facets, including facet-border rows where D wraps): x+ of every facet containing the
     pixel from its own facet-local data, then Lemma 1 and the dual update, against the
     GPU state in bench.py's launch configuration."""
-    pb = synth.make_config(k)
+    pb = full_config(k)
     facets = geometry.plan(pb.ny, pb.nx, pb.P, pb.fy, pb.fx, pb.overlap)
     w_max = float(pb.noise_w.max()) if pb.noise_w is not None else float(np.float32(pb.noise_w_scalar))
     tau = solver.default_tau(pb.psfs, pb.wy, pb.wx, w_max, pb.lam, pb.eps, pb.reg_kind, pb.gamma)
@@ -221,7 +222,7 @@ def test_iterate_full_size_band_pixels(k, count):
 def test_apply_c5_sampled(count):
     """c5 (32768^2, 32x32 grid of 127x127 PSFs, 8x8 facets) H / H^T on one GPU,
     sampled pixels including facet seams and image borders."""
-    pb = synth.make_config(5)
+    pb = full_config(5)
     rng = np.random.default_rng(55)
     x = (0.05 + rng.random((pb.ny, pb.nx), dtype=np.float32) * 0.5).astype(np.float32)
     op = Operator(pb.psfs, pb.wy, pb.wx)
@@ -285,7 +286,7 @@ def test_paper_shaped_c6_iterate_small():
 def test_graph_replay_equals_eager_full_size(k, monkeypatch):
     """The CUDA-graph replay of deblur_iterate (bench.py's launch configuration) and
     eager launches give bitwise identical states at full size."""
-    pb = synth.make_config(k)
+    pb = full_config(k)
     facets = geometry.plan(pb.ny, pb.nx, pb.P, pb.fy, pb.fx, pb.overlap)
     _, _, xs, us = _state(pb, facets, seed=400 + k)
     with D.Deblur.from_problem(pb) as dev:

@@ -21,6 +21,7 @@ import numpy as np
 import pytest
 
 import synth
+from tests.fullsize import full_config
 from paper_1705_06603_b200 import deblur as D
 
 pytestmark = pytest.mark.gpu
@@ -72,7 +73,7 @@ def load(name):
 def test_full_size_against_golden(name):
     g = load(name)
     k, iters = int(g["config"]), int(g["iters"])
-    pb = synth.make_config(k)
+    pb = full_config(k)
     assert synth.input_hash(pb) == str(g["input_hash"]), "inputs differ from the ones the golden file was made from"
     tau = float(g["tau"])
     trace_ref = g["trace"]                                   # [iters + 1, 4] at x^(0..iters)
@@ -112,7 +113,7 @@ def test_c5_objective_at_start_against_golden():
     a full c5 oracle iteration does not fit the host's memory, the iterate at c5 is checked
     at sampled interior and band pixels in test_gpu_fullsize.py)."""
     g = load("c5_obj0")
-    pb = synth.make_config(5)
+    pb = full_config(5)
     assert synth.input_hash(pb) == str(g["input_hash"])
     with D.Deblur.from_problem(pb) as dev:
         obj = dev.objective()

@@ -7,6 +7,7 @@ import pytest
 import scipy.signal
 
 import synth
+from tests.fullsize import full_config
 from oracle import Operator, from_problem
 from paper_1705_06603_b200 import deblur as D
 
@@ -165,7 +166,7 @@ def test_apply_full_size_sampled(k, count, path):
     checked on pixels the oracle evaluates one by one (1e5 random pixels at
     c4) plus dense 48x48 blocks across the structural boundaries: image corners, facet
     seams and shared bands, FFT tile and ragged-strip boundaries."""
-    pb = synth.make_config(k)
+    pb = full_config(k)
     rng = np.random.default_rng(k)
     x = (0.05 + rng.random((pb.ny, pb.nx), dtype=np.float32) * 0.5).astype(np.float32)
     r = rng.standard_normal((pb.my, pb.mx), dtype=np.float32)
