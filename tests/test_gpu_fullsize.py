@@ -300,3 +300,18 @@ def test_graph_replay_equals_eager_full_size(k, monkeypatch):
         xb, ub = dev.get_state()
     np.testing.assert_array_equal(xa, xb)
     np.testing.assert_array_equal(ua, ub)
+
+
+def test_long_run_c4_stable():
+    """200 full distributed iterations at c4 (four times the BASELINE count): every
+    objective finite, the objective falls from the A6 start, the iterate stays >= 0 and
+    the facets keep agreeing on their shared pixels (consensus max-difference bounded)."""
+    pb = full_config(4)
+    with D.Deblur.from_problem(pb) as dev:
+        tr = dev.iterate_traced(200)
+        x, _ = dev.get_state()
+        end = dev.objective()
+    assert np.all(np.isfinite(tr)) and np.all(np.isfinite(end))
+    assert end[0] < tr[0, 0] and tr[-1, 0] < tr[0, 0]
+    assert float(x.min()) >= 0.0
+    assert end[3] < 1.0 and np.max(tr[:, 3]) < 1.0
