@@ -219,6 +219,25 @@ DEBLUR_API deblur_status deblur_set_outer_iteration(deblur_t h, int32_t k);
  * A6 default).  noise weights are kept.  COLLECTIVE. */
 DEBLUR_API deblur_status deblur_reset(deblur_t h, const float *y, const float *x0);
 
+/* Pipelined jobs (a stream of observations of the same geometry, e.g. successive exposures):
+ * the next observation's upload and the previous image's download overlap the current
+ * job's iterations.
+ *   deblur_stage_y(h, y): start copying y (host [M_y][M_x]; page-locked for the copy to be
+ *     asynchronous) into the handle's second staging buffer on an upload stream; y must stay
+ *     valid until the next deblur_reset_staged / deblur_sync returns.
+ *   deblur_reset_staged(h, x0): restart from the staged observation (x0 host or NULL -> the
+ *     A6 default) -- the same state as deblur_reset(h, y, x0); returns without waiting for
+ *     the device (the next call on the handle is ordered after it).  DEBLUR_ESTATE if nothing
+ *     was staged.
+ *   deblur_get_image_async(h, x): the blended image (as deblur_get_image) into host x
+ *     (page-locked, [N_y][N_x]) on a download stream; x is complete when deblur_sync returns.
+ *     world == 1 only (else DEBLUR_ESTATE).
+ *   deblur_sync(h): wait for every outstanding upload, download and kernel of the handle. */
+DEBLUR_API deblur_status deblur_stage_y(deblur_t h, const float *y);
+DEBLUR_API deblur_status deblur_reset_staged(deblur_t h, const float *x0);
+DEBLUR_API deblur_status deblur_get_image_async(deblur_t h, float *x);
+DEBLUR_API deblur_status deblur_sync(deblur_t h);
+
 /* The Local-Solver step actually used (fp64 value from which the fp32 device
  * copy was rounded). */
 DEBLUR_API deblur_status deblur_get_step(deblur_t h, double *tau_used);

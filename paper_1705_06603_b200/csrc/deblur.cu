@@ -112,6 +112,15 @@ struct deblur_ctx {
     // persistent staging buffers for reset / get_image (allocated on first use)
     float *d_ystage = nullptr;            // staged observed image (bounding box of this rank's needs)
     int64_t ys_y0 = 0, ys_x0 = 0, ys_pitch = 1;
+    // pipelined jobs (deblur_stage_y / deblur_reset_staged / deblur_get_image_async): a second
+    // staging buffer filled on the upload stream while the current job iterates, and two image
+    // buffers downloaded on the download stream while the next job runs
+    float *d_ystage2 = nullptr;
+    cudaStream_t up_stream = nullptr, down_stream = nullptr;
+    cudaEvent_t ev_staged = nullptr, ev_yfree = nullptr, ev_blend = nullptr, ev_down[2] = {nullptr, nullptr};
+    bool staged = false;
+    float *d_image2[2] = {nullptr, nullptr};
+    int img_slot = 0;
     float *d_image = nullptr;
     // CUDA graphs of two full iterations (parity returns to its start), one per start parity
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
@@ -356,15 +365,21 @@ static deblur_status upload_slice(deblur_t h, float *dst, int64_t dpitch, const 
 // The observed image crosses PCIe once: the bounding box of what this rank's facets need
 // (their observed blocks O_f for y, and O_f dilated by c -- clipped -- for the A6 start)
 // is uploaded into a staging buffer; F.y and the A6 start are formed from it on the device.
-static deblur_status stage_y(deblur_t h, const float *y) {
+static void ystage_box(deblur_t h, int64_t &y0, int64_t &y1, int64_t &x0, int64_t &x1) {
     const Plan &pl = h->plan;
     const int c = (pl.P - 1) / 2;
-    int64_t y0 = pl.my, y1 = 0, x0 = pl.mx, x1 = 0;
+    y0 = pl.my; y1 = 0; x0 = pl.mx; x1 = 0;
     for (int id : h->local) {
         const FacetPlan &fp = pl.facets[id];
         y0 = std::min(y0, std::max<int64_t>(0, fp.ey0 - c)); y1 = std::max(y1, std::min<int64_t>(pl.my, fp.ey1 - c));
         x0 = std::min(x0, std::max<int64_t>(0, fp.ex0 - c)); x1 = std::max(x1, std::min<int64_t>(pl.mx, fp.ex1 - c));
     }
+}
+
+static deblur_status stage_y(deblur_t h, const float *y) {
+    const Plan &pl = h->plan;
+    int64_t y0, y1, x0, x1;
+    ystage_box(h, y0, y1, x0, x1);
     if (!h->d_ystage) CU(h->dalloc(&h->d_ystage, (size_t)pl.my * pl.mx));
     h->ys_y0 = y0; h->ys_x0 = x0; h->ys_pitch = std::max<int64_t>(1, x1 - x0);
     if (y1 > y0 && x1 > x0)
@@ -387,7 +402,7 @@ static deblur_status upload_y(deblur_t h) {
 
 // x0 given: upload its facet slices to x[0] and copy to u.  x0 == NULL: the A6
 // default computed on the device from the staged y.
-static deblur_status upload_state_x0(deblur_t h, const float *x0) {
+static deblur_status upload_state_x0(deblur_t h, const float *x0, bool sync = true) {
     const Plan &pl = h->plan;
     const int c = (pl.P - 1) / 2;
     for (size_t li = 0; li < h->local.size(); ++li) {
@@ -403,7 +418,7 @@ static deblur_status upload_state_x0(deblur_t h, const float *x0) {
         }
     }
     h->par = 0;
-    CU(cudaStreamSynchronize(h->stream));
+    if (sync) CU(cudaStreamSynchronize(h->stream));
     return DEBLUR_OK;
 }
 
@@ -599,6 +614,8 @@ deblur_status deblur_destroy(deblur_t h) {
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->cstream) cudaStreamSynchronize(h->cstream);
+    if (h->up_stream) cudaStreamSynchronize(h->up_stream);
+    if (h->down_stream) cudaStreamSynchronize(h->down_stream);
     for (auto &g : h->gexec)
         if (g) { cudaGraphExecDestroy(g); g = nullptr; }
     if (h->fft) { fft_destroy(h->fft); h->fft = nullptr; }
@@ -607,6 +624,10 @@ deblur_status deblur_destroy(deblur_t h) {
     for (auto &p : h->pending) { h->ev_pool.push_back(p.a); h->ev_pool.push_back(p.b); }
     for (auto e : h->ev_pool) cudaEventDestroy(e);
     for (void *p : h->allocs) cudaFree(p);
+    for (cudaEvent_t e : {h->ev_staged, h->ev_yfree, h->ev_blend, h->ev_down[0], h->ev_down[1]})
+        if (e) cudaEventDestroy(e);
+    if (h->up_stream) cudaStreamDestroy(h->up_stream);
+    if (h->down_stream) cudaStreamDestroy(h->down_stream);
     if (h->ev_upd) cudaEventDestroy(h->ev_upd);
     if (h->ev_cons) cudaEventDestroy(h->ev_cons);
     if (h->cstream) cudaStreamDestroy(h->cstream);
@@ -671,6 +692,10 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
     CUC(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
     CUC(cudaEventCreateWithFlags(&h->ev_upd, cudaEventDisableTiming));
     CUC(cudaEventCreateWithFlags(&h->ev_cons, cudaEventDisableTiming));
+    CUC(cudaStreamCreateWithFlags(&h->up_stream, cudaStreamNonBlocking));
+    CUC(cudaStreamCreateWithFlags(&h->down_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t *e : {&h->ev_staged, &h->ev_yfree, &h->ev_blend, &h->ev_down[0], &h->ev_down[1]})
+        CUC(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
 
     // conv path (A: measured crossover)
     int path = p->conv_path;
@@ -1625,6 +1650,78 @@ deblur_status deblur_reset(deblur_t h, const float *y, const float *x0) {
     if ((s = upload_y(h)) != DEBLUR_OK) return s;
     h->vm.k_outer = 0;                                // a fresh solve: VMLM-B budget schedule restarts
     return upload_state_x0(h, x0);
+}
+
+// ---------------------------------------------------------------- pipelined jobs
+deblur_status deblur_stage_y(deblur_t h, const float *y) {
+    deblur_status s = check_state(h);
+    if (s != DEBLUR_OK) return s;
+    if (!y) return h->fail(DEBLUR_EINVAL, "y is NULL");
+    const Plan &pl = h->plan;
+    if (!h->d_ystage2) CU(h->dalloc(&h->d_ystage2, (size_t)pl.my * pl.mx));
+    int64_t y0, y1, x0, x1;
+    ystage_box(h, y0, y1, x0, x1);
+    // the buffer may still feed the previous reset_staged's device copies
+    CU(cudaStreamWaitEvent(h->up_stream, h->ev_yfree, 0));
+    if (y1 > y0 && x1 > x0)
+        CU(cudaMemcpy2DAsync(h->d_ystage2, std::max<int64_t>(1, x1 - x0) * 4, y + y0 * pl.mx + x0, pl.mx * 4,
+                             (x1 - x0) * 4, y1 - y0, cudaMemcpyHostToDevice, h->up_stream));
+    CU(cudaEventRecord(h->ev_staged, h->up_stream));
+    h->staged = true;
+    return DEBLUR_OK;
+}
+
+deblur_status deblur_reset_staged(deblur_t h, const float *x0) {
+    deblur_status s = check_state(h);
+    if (s != DEBLUR_OK) return s;
+    if (!h->staged) return h->fail(DEBLUR_ESTATE, "no observation staged (deblur_stage_y)");
+    int64_t y0, y1, xa, x1;
+    ystage_box(h, y0, y1, xa, x1);
+    CU(cudaStreamWaitEvent(h->stream, h->ev_staged, 0));
+    if (!h->d_ystage) CU(h->dalloc(&h->d_ystage, (size_t)h->plan.my * h->plan.mx));
+    std::swap(h->d_ystage, h->d_ystage2);
+    h->ys_y0 = y0; h->ys_x0 = xa; h->ys_pitch = std::max<int64_t>(1, x1 - xa);
+    h->staged = false;
+    if ((s = upload_y(h)) != DEBLUR_OK) return s;
+    h->vm.k_outer = 0;
+    if ((s = upload_state_x0(h, x0, false)) != DEBLUR_OK) return s;
+    CU(cudaEventRecord(h->ev_yfree, h->stream));       // the other buffer may be refilled after this
+    return DEBLUR_OK;
+}
+
+deblur_status deblur_get_image_async(deblur_t h, float *x) {
+    deblur_status s = check_state(h);
+    if (s != DEBLUR_OK) return s;
+    if (h->world != 1) return h->fail(DEBLUR_ESTATE, "get_image_async needs world == 1 (use deblur_get_image)");
+    if (!x) return h->fail(DEBLUR_EINVAL, "x is NULL");
+    const Plan &pl = h->plan;
+    const int b = h->img_slot;
+    h->img_slot ^= 1;
+    if (!h->d_image2[b]) CU(h->dalloc(&h->d_image2[b], (size_t)pl.ny * pl.nx));
+    float *img = h->d_image2[b];
+    CU(cudaStreamWaitEvent(h->stream, h->ev_down[b], 0));   // its previous download is done
+    CU(cudaMemsetAsync(img, 0, (size_t)pl.ny * pl.nx * 4, h->stream));
+    float *wsum = nullptr;
+    if (h->per_node) {
+        if (!h->d_wsum) CU(h->dalloc(&h->d_wsum, (size_t)pl.ny * pl.nx));
+        wsum = h->d_wsum;
+        CU(cudaMemsetAsync(wsum, 0, (size_t)pl.ny * pl.nx * 4, h->stream));
+    }
+    for (size_t li = 0; li < h->local.size(); ++li) CU(launch_blend(h->fh[li], h->par, img, wsum, pl.nx, h->stream));
+    if (wsum) CU(launch_normalize(img, wsum, (int64_t)pl.ny * pl.nx, h->stream));
+    CU(cudaEventRecord(h->ev_blend, h->stream));
+    CU(cudaStreamWaitEvent(h->down_stream, h->ev_blend, 0));
+    CU(cudaMemcpyAsync(x, img, (size_t)pl.ny * pl.nx * 4, cudaMemcpyDeviceToHost, h->down_stream));
+    CU(cudaEventRecord(h->ev_down[b], h->down_stream));
+    return DEBLUR_OK;
+}
+
+deblur_status deblur_sync(deblur_t h) {
+    deblur_status s = check_state(h);
+    if (s != DEBLUR_OK) return s;
+    CU(cudaStreamSynchronize(h->up_stream));
+    CU(cudaStreamSynchronize(h->down_stream));
+    return finish(h);
 }
 
 deblur_status deblur_get_outer_iteration(deblur_t h, int32_t *k) {

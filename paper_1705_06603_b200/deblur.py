@@ -88,6 +88,10 @@ def lib():
             "deblur_get_outer_iteration": ([h, _ip], ctypes.c_int),
             "deblur_set_outer_iteration": ([h, ctypes.c_int32], ctypes.c_int),
             "deblur_reset": ([h, _fp, _fp], ctypes.c_int),
+            "deblur_stage_y": ([h, _fp], ctypes.c_int),
+            "deblur_reset_staged": ([h, _fp], ctypes.c_int),
+            "deblur_get_image_async": ([h, _fp], ctypes.c_int),
+            "deblur_sync": ([h], ctypes.c_int),
             "deblur_get_step": ([h, _dp], ctypes.c_int),
             "deblur_set_profiling": ([h, ctypes.c_int32], ctypes.c_int),
             "deblur_kernel_stats": ([h, _ip, _lp, _dp], ctypes.c_int),
@@ -112,6 +116,7 @@ EXPORTED = ["deblur_nccl_id", "deblur_create", "deblur_destroy", "deblur_apply_H
             "deblur_apply_H_device", "deblur_apply_HT_device", "deblur_iterate", "deblur_iterate_traced",
             "deblur_objective", "deblur_get_image", "deblur_state_size", "deblur_get_state", "deblur_set_state",
             "deblur_get_outer_iteration", "deblur_set_outer_iteration", "deblur_reset",
+            "deblur_stage_y", "deblur_reset_staged", "deblur_get_image_async", "deblur_sync",
             "deblur_get_step", "deblur_set_profiling", "deblur_kernel_stats", "deblur_kernel_name",
             "deblur_reset_stats", "deblur_kernel_work", "deblur_get_conv_path", "deblur_get_stream", "deblur_plan_facets", "deblur_plan_messages",
             "deblur_last_error"]
@@ -317,6 +322,24 @@ class Deblur:
         y = _f32(y)
         x0 = None if x0 is None else _f32(x0)
         self._c(self._lib.deblur_reset(self._h, _ptr(y), _ptr(x0)))
+
+    # --- pipelined jobs (the caller keeps y / out alive until sync()) ---------------------
+    def stage_y(self, y):
+        y = np.asarray(y)
+        assert y.dtype == np.float32 and y.flags.c_contiguous and y.shape == (self.my, self.mx)
+        self._staged_y = y
+        self._c(self._lib.deblur_stage_y(self._h, _ptr(y)))
+
+    def reset_staged(self, x0=None):
+        x0 = None if x0 is None else _f32(x0)
+        self._c(self._lib.deblur_reset_staged(self._h, _ptr(x0)))
+
+    def get_image_async(self, out):
+        assert out.dtype == np.float32 and out.shape == (self.ny, self.nx) and out.flags.c_contiguous
+        self._c(self._lib.deblur_get_image_async(self._h, _ptr(out)))
+
+    def sync(self):
+        self._c(self._lib.deblur_sync(self._h))
 
     @property
     def tau(self) -> float:

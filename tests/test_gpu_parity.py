@@ -516,3 +516,31 @@ def test_vmlmb_checkpoint_resume_with_outer_iteration():
             dev.set_state(xs[:-1], us)
     np.testing.assert_array_equal(xa, xb)
     np.testing.assert_array_equal(ua, ub)
+
+
+@pytest.mark.parametrize("path", PATHS, ids=["direct", "fft"])
+def test_pipelined_jobs_equal_serial_jobs(path):
+    """deblur_stage_y / reset_staged / get_image_async (the next observation uploaded and
+    the previous image downloaded while a job iterates) give exactly the serial jobs'
+    images: three different observations back to back."""
+    pb = synth.make_config(2, n=300, facets=(3, 2), overlap=40)
+    ys = [np.ascontiguousarray((pb.y * s + 0.01 * i).astype(np.float32)) for i, s in enumerate((1.0, 0.7, 1.3))]
+    with D.Deblur.from_problem(pb, conv_path=path) as dev:
+        ref = []
+        for y in ys:
+            dev.reset(y)
+            dev.iterate(5)
+            ref.append(dev.get_image())
+        outs = [np.empty((pb.ny, pb.nx), np.float32) for _ in ys]
+        dev.stage_y(ys[0])
+        for j in range(len(ys)):
+            dev.reset_staged()
+            if j + 1 < len(ys):
+                dev.stage_y(ys[j + 1])
+            dev.iterate(5)
+            dev.get_image_async(outs[j])
+        dev.sync()
+        with pytest.raises(D.DeblurError):
+            dev.reset_staged()                    # nothing staged
+    for a, b in zip(outs, ref):
+        np.testing.assert_array_equal(a, b)
