@@ -89,3 +89,15 @@ def test_fft_and_direct_iterates_agree_at_scale():
     assert rel_l2(out[0][0], out[1][0]) <= IT_TOL
     for i in range(3):
         assert abs(out[0][1][i] - out[1][1][i]) <= OBJ_TOL * abs(out[1][1][i])
+
+
+def test_c_abi_from_plain_c():
+    """examples/c_demo.c drives create / apply_H / reset / objective / iterate / get_image /
+    destroy from C (no Python binding): it exits 0 when the objective fell."""
+    import os
+    import subprocess
+    import __graft_entry__ as g
+    exe = g.build_c_demo()
+    r = subprocess.run([exe, "10"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "objective" in r.stdout and "SNR" in r.stdout
