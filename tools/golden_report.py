@@ -46,7 +46,7 @@ def report(name):
     out["img_rel_l2"] = rel_l2(img[g["img_i"], g["img_j"]], g["img"])
     ref = g["trace"]
     dev_tr = np.vstack([tr[:, :3], np.array(obj_end[:3])[None]])
-    out["objective_max_rel"] = float(np.max(np.abs(dev_tr - ref[:, :3]) / np.abs(ref[:, :3])))
+    out["objective_max_rel"] = float(np.nanmax(np.abs(dev_tr - ref[:, :3]) / np.abs(ref[:, :3])))
     out["objective_first_last"] = [float(ref[0, 0]), float(ref[-1, 0])]
     print(json.dumps(out), flush=True)
 

@@ -17,6 +17,8 @@ geometry and stores
 
 Usage:  python tools/make_golden.py 3 100      (c3, 100 iterations: ~2 h on 8 cores)
         python tools/make_golden.py 4 2        (c4, a stated 2-iteration prefix)
+        python tools/make_golden.py 4 50 --checkpoints 10,20,30,40 --objective-every 5
+                                               (c4, the BASELINE 50 iterations, a file every 10)
         python tools/make_golden.py 5 0 --objective-only
                                                (c5: Eq. (4) at the A6 start, facet by facet; a full
                                                 c5 oracle iteration needs > 62 GB of host memory)
@@ -118,6 +120,10 @@ def main():
     ap.add_argument("--n-random", type=int, default=60000)
     ap.add_argument("--n-class", type=int, default=20000)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--checkpoints", default="",
+                    help="comma-separated iteration counts at which a golden file is also written")
+    ap.add_argument("--objective-every", type=int, default=1,
+                    help="evaluate Eq. (4) at every n-th iterate (and at each checkpoint)")
     ap.add_argument("--objective-only", action="store_true",
                     help="only Eq. (4) at the A6 start, evaluated facet by facet (no global arrays)")
     a = ap.parse_args()
@@ -135,24 +141,31 @@ def main():
     idx = sample_state(facets, rng, a.n_random, a.n_class)
     gi = rng.integers(0, pb.ny, 20000)
     gj = rng.integers(0, pb.nx, 20000)
-    trace = np.zeros((a.iters + 1, 4))
+    # a file per checkpoint (the last one = iters); the objective at every `objective_every`-th
+    # iterate and at each checkpoint, NaN rows elsewhere (the test skips them)
+    checkpoints = sorted({int(c) for c in a.checkpoints.split(",") if c} | {a.iters}) if a.checkpoints else [a.iters]
+    trace = np.full((a.iters + 1, 4), np.nan)
     for it in range(a.iters + 1):
-        t = time.time()
-        trace[it] = orc.objective()
-        to = time.time() - t
+        to = 0.0
+        if it % a.objective_every == 0 or it in checkpoints:
+            t = time.time()
+            trace[it] = orc.objective()
+            to = time.time() - t
+        if it in checkpoints:
+            xs, us = orc.state()
+            img = orc.image()
+            out = (a.out if (a.out and it == a.iters) else
+                   os.path.join(GOLDEN, f"c{a.k}_it{it}.npz"))
+            np.savez_compressed(out, config=a.k, iters=it, input_hash=h, tau=orc.tau, trace=trace[:it + 1],
+                                idx=idx, x=xs[idx], u=us[idx], img_i=gi, img_j=gj, img=img[gi, gj],
+                                made_by="tools/make_golden.py (oracle/ + synth/ only)")
+            del xs, us, img
+            print(f"wrote {out}: {idx.size} state samples, {time.time() - t0:.0f} s total", flush=True)
         if it < a.iters:
             t = time.time()
             orc.iterate(1)
             print(f"  it {it}: objective {trace[it, 0]:.9e} ({to:.0f} s), iterate {time.time() - t:.0f} s",
                   flush=True)
-    xs, us = orc.state()
-    img = orc.image()
-    out = a.out or os.path.join(GOLDEN, f"c{a.k}_it{a.iters}.npz")
-    np.savez_compressed(out, config=a.k, iters=a.iters, input_hash=h, tau=orc.tau, trace=trace,
-                        idx=idx, x=xs[idx], u=us[idx], img_i=gi, img_j=gj, img=img[gi, gj],
-                        made_by="tools/make_golden.py (oracle/ + synth/ only)")
-    print(f"wrote {out}: {idx.size} state samples, {time.time() - t0:.0f} s total", flush=True)
-
 
 if __name__ == "__main__":
     main()
