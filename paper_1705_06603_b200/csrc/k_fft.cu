@@ -120,22 +120,52 @@ __device__ __forceinline__ void dft4(float2 &a0, float2 &a1, float2 &a2, float2 
     a3 = csub(d0, d1);
 }
 
+// Radix-8 DFT from its first-level pair sums / differences: s0, d0 = a0 +- a4 and
+// s1, m1 = a2 +- a6 of the even inputs, S0, D0 = a1 +- a5 and S1, M1 = a3 +- a7 of the odd
+// ones.  The w8^1, w8^3 products (r = sqrt(1/2)) are folded into the last additions as
+// FMAs (6 instructions per product-and-butterfly instead of 8).
+template <int SIGN>
+__device__ __forceinline__ void dft8_tail(float2 &v0, float2 &v1, float2 &v2, float2 &v3, float2 &v4, float2 &v5,
+                                          float2 &v6, float2 &v7, float2 s0, float2 d0, float2 s1, float2 m1,
+                                          float2 S0, float2 D0, float2 S1, float2 M1) {
+    const float r = 0.70710678118654752f;
+    const float2 d1 = rot90<SIGN>(m1), D1 = rot90<SIGN>(M1);
+    const float2 e0 = cadd(s0, s1), e2 = csub(s0, s1), e1 = cadd(d0, d1), e3 = csub(d0, d1);
+    const float2 o0 = cadd(S0, S1), o2 = rot90<SIGN>(csub(S0, S1)), o1 = cadd(D0, D1), o3 = csub(D0, D1);
+    v0 = cadd(e0, o0); v4 = csub(e0, o0);
+    v2 = cadd(e2, o2); v6 = csub(e2, o2);
+    // w8^1 o1 = r (o1.x - SIGN o1.y, o1.y + SIGN o1.x)
+    const float p1 = o1.x - SIGN * o1.y, q1 = o1.y + SIGN * o1.x;
+    v1 = make_float2(__fmaf_rn(r, p1, e1.x), __fmaf_rn(r, q1, e1.y));
+    v5 = make_float2(__fmaf_rn(-r, p1, e1.x), __fmaf_rn(-r, q1, e1.y));
+    // w8^3 o3 = (-r (o3.x + SIGN o3.y), r (SIGN o3.x - o3.y))
+    const float p3 = o3.x + SIGN * o3.y, q3 = SIGN * o3.x - o3.y;
+    v3 = make_float2(__fmaf_rn(-r, p3, e3.x), __fmaf_rn(r, q3, e3.y));
+    v7 = make_float2(__fmaf_rn(r, p3, e3.x), __fmaf_rn(-r, q3, e3.y));
+}
+
 template <int SIGN>
 __device__ __forceinline__ void dft8(float2 &v0, float2 &v1, float2 &v2, float2 &v3, float2 &v4, float2 &v5,
                                      float2 &v6, float2 &v7) {
-    const float r = 0.70710678118654752f;
-    float2 e0 = v0, e1 = v2, e2 = v4, e3 = v6;
-    float2 o0 = v1, o1 = v3, o2 = v5, o3 = v7;
-    dft4<SIGN>(e0, e1, e2, e3);
-    dft4<SIGN>(o0, o1, o2, o3);
-    // w8^1 = (r, SIGN r), w8^2 = SIGN i, w8^3 = (-r, SIGN r)
-    const float2 t1 = make_float2(r * (o1.x - SIGN * o1.y), r * (o1.y + SIGN * o1.x));
-    const float2 t2 = rot90<SIGN>(o2);
-    const float2 t3 = make_float2(-r * (o3.x + SIGN * o3.y), r * (SIGN * o3.x - o3.y));
-    v0 = cadd(e0, o0); v4 = csub(e0, o0);
-    v1 = cadd(e1, t1); v5 = csub(e1, t1);
-    v2 = cadd(e2, t2); v6 = csub(e2, t2);
-    v3 = cadd(e3, t3); v7 = csub(e3, t3);
+    dft8_tail<SIGN>(v0, v1, v2, v3, v4, v5, v6, v7, cadd(v0, v4), csub(v0, v4), cadd(v2, v6), csub(v2, v6),
+                    cadd(v1, v5), csub(v1, v5), cadd(v3, v7), csub(v3, v7));
+}
+
+// a_n * w_n (w real) followed by the radix-8 DFT, the weights folded into the first-level
+// sums: w_a a + w_b b = fma(w_b, b, w_a a) (3 instructions per component pair instead of 4)
+__device__ __forceinline__ void wpair(float2 a, float2 b, float wa, float wb, float2 &s, float2 &d) {
+    const float2 t = make_float2(wa * a.x, wa * a.y);
+    s = make_float2(__fmaf_rn(wb, b.x, t.x), __fmaf_rn(wb, b.y, t.y));
+    d = make_float2(__fmaf_rn(-wb, b.x, t.x), __fmaf_rn(-wb, b.y, t.y));
+}
+template <int SIGN>
+__device__ __forceinline__ void dft8w(float2 *v, const float (&w)[8]) {
+    float2 s0, d0, s1, m1, S0, D0, S1, M1;
+    wpair(v[0], v[4], w[0], w[4], s0, d0);
+    wpair(v[2], v[6], w[2], w[6], s1, m1);
+    wpair(v[1], v[5], w[1], w[5], S0, D0);
+    wpair(v[3], v[7], w[3], w[7], S1, M1);
+    dft8_tail<SIGN>(v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], s0, d0, s1, m1, S0, D0, S1, M1);
 }
 
 // Radix plans.  For L >= 64 the first and the last stage are radix 8, so the
@@ -723,7 +753,9 @@ __global__ void __launch_bounds__(GC<S>::NTH) k_cols(FftArgs A, int mode, const 
         const int np = td.p1 - td.p0 + 1, nq = td.q1 - td.q0 + 1;
         for (int idx = tid; idx < np * S; idx += NTH) {
             const int pi = idx / S, i = idx - pi * S;
-            wys_all[idx] = (td.y0 + i < Fd.ny) ? __ldg(A.wy + (size_t)(td.p0 + pi) * A.Ny + Fd.ey0 + td.y0 + i) : 0.f;
+            // (H^T weights its outputs: rows >= T, which are dropped, get weight 0)
+            wys_all[idx] = (td.y0 + i < Fd.ny && (mode == 0 || i < T))
+                               ? __ldg(A.wy + (size_t)(td.p0 + pi) * A.Ny + Fd.ey0 + td.y0 + i) : 0.f;
         }
         for (int idx = tid; idx < np * nq; idx += NTH) {
             const int pi = idx / nq, qi = idx - pi * nq;
@@ -909,7 +941,7 @@ __global__ void __launch_bounds__(GC<S>::NTH) k_cols(FftArgs A, int mode, const 
 #pragma unroll
                 for (int r = 0; r < SL::R; ++r) {
                     const int n = SL::out_n(j, r);
-                    const float wv = (n < T) ? wys[n] : 0.f;
+                    const float wv = wys[n];
                     float2 &o = acc[i * SL::R + r];
                     o = make_float2(o.x + wv * v[i * SL::R + r].x, o.y + wv * v[i * SL::R + r].y);
                 }
@@ -1016,7 +1048,9 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
     extern __shared__ __align__(16) float2 sm2[];
     // hbuf first, 128-byte aligned: the PSF-spectrum chunk (S x NB, pair-interleaved) lands there
     // by one TMA tensor copy per (p, q)
-    float2 *hbuf = reinterpret_cast<float2 *>((reinterpret_cast<uintptr_t>(sm2) + 127) & ~static_cast<uintptr_t>(127));
+    // (offsets from sm2, not integer round trips, so every access below stays a 32-bit
+    // shared-window LDS / STS instead of a generic 64-bit LD / ST)
+    float2 *hbuf = sm2 + (((128u - ((uint32_t)__cvta_generic_to_shared(sm2) & 127u)) & 127u) >> 3);
     float2 *Wsm = hbuf + S * NB;     // S/2 twiddles
     float2 *work = Wsm + COLS_TM_TW; // NB x CS
     float2 *hnq = work + NB * CS;    // S: Nyquist column of the PSF spectrum (chunk 0)
@@ -1024,7 +1058,7 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
     float *wys_all = reinterpret_cast<float *>(nyq + S);
     int *slot_s = reinterpret_cast<int *>(wys_all + (size_t)A.NP * S);
     uint32_t *tm_slot = reinterpret_cast<uint32_t *>(slot_s + A.NP * A.NQ);
-    uint64_t *hbar = reinterpret_cast<uint64_t *>((reinterpret_cast<uintptr_t>(tm_slot + 1) + 7) & ~static_cast<uintptr_t>(7));
+    uint64_t *hbar = reinterpret_cast<uint64_t *>(tm_slot + ((((uint32_t)__cvta_generic_to_shared(tm_slot + 1)) & 7u) ? 2 : 1));
     const int tid = threadIdx.x, warp = tid >> 5;
     constexpr uint32_t HBYTES = S * NB * 8;
     uint32_t hphase = 0;
@@ -1056,7 +1090,9 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
         const int np = td.p1 - td.p0 + 1, nq = td.q1 - td.q0 + 1;
         for (int idx = tid; idx < np * S; idx += NTH) {
             const int pi = idx / S, i = idx - pi * S;
-            wys_all[idx] = (td.y0 + i < Fd.ny) ? __ldg(A.wy + (size_t)(td.p0 + pi) * A.Ny + Fd.ey0 + td.y0 + i) : 0.f;
+            // (H^T weights its outputs: rows >= T, which are dropped, get weight 0)
+            wys_all[idx] = (td.y0 + i < Fd.ny && (mode == 0 || i < T))
+                               ? __ldg(A.wy + (size_t)(td.p0 + pi) * A.Ny + Fd.ey0 + td.y0 + i) : 0.f;
         }
         for (int idx = tid; idx < np * nq; idx += NTH) {
             const int pi = idx / nq, qi = idx - pi * nq;
@@ -1147,19 +1183,20 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
                 tma_hhat(p, q);                    // lands under the FFT below
                 const float *wys = wys_all + (size_t)(p - td.p0) * S;
                 if (p != td.p0) tm_get<E>(t_in, v);
+                static_assert(S0::R == 8 && S0::Ns == 1, "untwiddled radix-8 first stage");
 #pragma unroll
                 for (int i = 0; i < S0::BPT; i += 2) {
                     int t, j;
                     S0::bj(i, tid, t, j);
+                    float w0[8], w1[8];
 #pragma unroll
                     for (int r = 0; r < S0::R; ++r) {
-                        const int n = S0::in_n(j, r);
-                        const float2 wv = *reinterpret_cast<const float2 *>(wys + n);
-                        v[i * S0::R + r].x *= wv.x; v[i * S0::R + r].y *= wv.x;
-                        v[(i + 1) * S0::R + r].x *= wv.y; v[(i + 1) * S0::R + r].y *= wv.y;
+                        const float2 wv = *reinterpret_cast<const float2 *>(wys + S0::in_n(j, r));
+                        w0[r] = wv.x;
+                        w1[r] = wv.y;
                     }
-                    S0::template bfly<-1>(&v[i * S0::R], j, Wsm, S);
-                    S0::template bfly<-1>(&v[(i + 1) * S0::R], j + 1, Wsm, S);
+                    dft8w<-1>(&v[i * S0::R], w0);          // (wy_p . A_q) -> first stage
+                    dft8w<-1>(&v[(i + 1) * S0::R], w1);
                 }
                 F::template middle_open<-1>(work, v, tid, tw);
                 if (pk) {
@@ -1206,10 +1243,12 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
 #pragma unroll
                         for (int r = 0; r < SL::R; ++r) {
                             const float2 hv = hbuf[hb_idx<NB>(SL::out_n(j, r), t)];
-                            const float2 p0 = cmul(v[i * SL::R + r], hv);
+                            const float2 x = v[i * SL::R + r];
                             const int e = (i2 * SL::R + r) * 2;
                             float2 a0 = first ? make_float2(0.f, 0.f) : make_float2(__uint_as_float(a[e]), __uint_as_float(a[e + 1]));
-                            a0 = cadd(a0, p0);
+                            // a0 += x . hv as four FMAs
+                            a0.x = __fmaf_rn(x.x, hv.x, __fmaf_rn(-x.y, hv.y, a0.x));
+                            a0.y = __fmaf_rn(x.x, hv.y, __fmaf_rn(x.y, hv.x, a0.y));
                             a[e] = __float_as_uint(a0.x);
                             a[e + 1] = __float_as_uint(a0.y);
                         }
@@ -1306,7 +1345,7 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
 #pragma unroll
                         for (int r = 0; r < SL::R; ++r) {
                             const int n = SL::out_n(j, r);
-                            const float wv = (n < T) ? wys[n] : 0.f;
+                            const float wv = wys[n];
                             const int e = (i2 * SL::R + r) * 2;
                             float2 o = first ? make_float2(0.f, 0.f) : make_float2(__uint_as_float(a[e]), __uint_as_float(a[e + 1]));
                             o.x += wv * v[i * SL::R + r].x;
