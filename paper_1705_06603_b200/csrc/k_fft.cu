@@ -408,6 +408,12 @@ __device__ __forceinline__ void tm_st16(uint32_t ta, const uint32_t (&r)[16]) {
 __device__ __forceinline__ void tm_ld16(uint32_t ta, uint32_t (&r)[16]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];\n" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]) : "r"(ta) : "memory");
 }
+__device__ __forceinline__ void tm_st8(uint32_t ta, const uint32_t (&r)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%8], {%0, %1, %2, %3, %4, %5, %6, %7};\n" :: "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(ta) : "memory");
+}
+__device__ __forceinline__ void tm_ld8(uint32_t ta, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]) : "r"(ta) : "memory");
+}
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
@@ -1168,8 +1174,17 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
     };
     float2 v[E];
 
+    // the accumulator starts at zero in TMEM, so every (p, q) step is load-FMA-store (no
+    // first-step selects)
+    auto acc_zero = [&]() {
+        uint32_t z[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) z[e] = 0u;
+        tm_st16(t_acc, z);
+        tm_st16(t_acc + 16, z);
+    };
     if (mode == 0) {
-        bool first = true;
+        acc_zero();
         for (int q = td.q0; q <= td.q1; ++q) {
             load_in(base + (int64_t)(q - td.q0) * S * LDF, v);
             tm_put<E>(t_in, v);
@@ -1228,43 +1243,39 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
                         }
                     }
                 }
-                // acc += v . Hhat, in two halves of 8 complex (16 TMEM columns each)
+                // acc += v . Hhat in two halves h = last-stage radix outputs r in [4h, 4h + 4) of
+                // both butterflies (j, j + 1): their spectrum values at rows (n, n + 1) are one
+                // conflict-free 16-byte load (8-byte loads of one member each were 2-way bank
+                // conflicted); the halves' accumulators are two 8-column TMEM runs each
+                static_assert(SL::BPT == 2 && SL::R == 8, "two radix-8 butterflies per thread");
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    uint32_t a[16];
-                    if (!first) { tm_ld16(t_acc + 16 * h, a); tm_wait_ld(); }
-                    // half h = butterflies [h BPT/2, (h+1) BPT/2): 8-byte loads of their own
-                    // spectrum values (a half never holds both members of a 16-byte pair)
+                    uint32_t a0[8], a1[8];
+                    tm_ld8(t_acc + 8 * h, a0);
+                    tm_ld8(t_acc + 16 + 8 * h, a1);
+                    tm_wait_ld();
+                    int t, j;
+                    SL::bj(0, tid, t, j);
 #pragma unroll
-                    for (int i2 = 0; i2 < SL::BPT / 2; ++i2) {
-                        const int i = h * (SL::BPT / 2) + i2;
-                        int t, j;
-                        SL::bj(i, tid, t, j);
-#pragma unroll
-                        for (int r = 0; r < SL::R; ++r) {
-                            const float2 hv = hbuf[hb_idx<NB>(SL::out_n(j, r), t)];
-                            const float2 x = v[i * SL::R + r];
-                            const int e = (i2 * SL::R + r) * 2;
-                            float2 a0 = first ? make_float2(0.f, 0.f) : make_float2(__uint_as_float(a[e]), __uint_as_float(a[e + 1]));
-                            // a0 += x . hv as four FMAs
-                            a0.x = __fmaf_rn(x.x, hv.x, __fmaf_rn(-x.y, hv.y, a0.x));
-                            a0.y = __fmaf_rn(x.x, hv.y, __fmaf_rn(x.y, hv.x, a0.y));
-                            a[e] = __float_as_uint(a0.x);
-                            a[e + 1] = __float_as_uint(a0.y);
-                        }
+                    for (int rr = 0; rr < 4; ++rr) {
+                        const int r = 4 * h + rr;
+                        const float4 hh = ld4(hbuf + hb_idx<NB>(SL::out_n(j, r), t));
+                        const float2 x0 = v[r], x1 = v[SL::R + r];
+                        float ax = __uint_as_float(a0[2 * rr]), ay = __uint_as_float(a0[2 * rr + 1]);
+                        a0[2 * rr] = __float_as_uint(__fmaf_rn(x0.x, hh.x, __fmaf_rn(-x0.y, hh.y, ax)));
+                        a0[2 * rr + 1] = __float_as_uint(__fmaf_rn(x0.x, hh.y, __fmaf_rn(x0.y, hh.x, ay)));
+                        ax = __uint_as_float(a1[2 * rr]);
+                        ay = __uint_as_float(a1[2 * rr + 1]);
+                        a1[2 * rr] = __float_as_uint(__fmaf_rn(x1.x, hh.z, __fmaf_rn(-x1.y, hh.w, ax)));
+                        a1[2 * rr + 1] = __float_as_uint(__fmaf_rn(x1.x, hh.w, __fmaf_rn(x1.y, hh.z, ay)));
                     }
-                    tm_st16(t_acc + 16 * h, a);
+                    tm_st8(t_acc + 8 * h, a0);
+                    tm_st8(t_acc + 16 + 8 * h, a1);
                 }
                 tm_wait_st();
-                first = false;
             }
         }
-        if (first) {
-#pragma unroll
-            for (int e = 0; e < E; ++e) v[e] = make_float2(0.f, 0.f);
-        } else {
-            tm_get<E>(t_acc, v);
-        }
+        tm_get<E>(t_acc, v);
         // inverse DFT along y; the accumulator sits at stage-0 input positions
 #pragma unroll
         for (int i = 0; i < S0::BPT; ++i) {
@@ -1307,7 +1318,8 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
         tm_wait_st();
         float2 *Bbase = base + (int64_t)S * LDF + f0;
         for (int q = td.q0; q <= td.q1; ++q) {
-            bool first = true;
+            acc_zero();
+            tm_wait_st();
             for (int p = td.p0; p <= td.p1; ++p) {
                 const float *wys = wys_all + (size_t)(p - td.p0) * S;
                 tm_get<E>(t_in, v);
@@ -1336,7 +1348,8 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     uint32_t a[16];
-                    if (!first) { tm_ld16(t_acc + 16 * h, a); tm_wait_ld(); }
+                    tm_ld16(t_acc + 16 * h, a);
+                    tm_wait_ld();
 #pragma unroll
                     for (int i2 = 0; i2 < SL::BPT / 2; ++i2) {
                         const int i = h * (SL::BPT / 2) + i2;
@@ -1347,7 +1360,7 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
                             const int n = SL::out_n(j, r);
                             const float wv = wys[n];
                             const int e = (i2 * SL::R + r) * 2;
-                            float2 o = first ? make_float2(0.f, 0.f) : make_float2(__uint_as_float(a[e]), __uint_as_float(a[e + 1]));
+                            float2 o = make_float2(__uint_as_float(a[e]), __uint_as_float(a[e + 1]));
                             o.x += wv * v[i * SL::R + r].x;
                             o.y += wv * v[i * SL::R + r].y;
                             a[e] = __float_as_uint(o.x); a[e + 1] = __float_as_uint(o.y);
@@ -1356,14 +1369,8 @@ __global__ void __launch_bounds__(32 * COLS_TM_NB, COLS_TM_MINB) k_cols_tm(FftAr
                     tm_st16(t_acc + 16 * h, a);
                 }
                 tm_wait_st();
-                first = false;
             }
-            if (first) {
-#pragma unroll
-                for (int e = 0; e < E; ++e) v[e] = make_float2(0.f, 0.f);
-            } else {
-                tm_get<E>(t_acc, v);
-            }
+            tm_get<E>(t_acc, v);
             float2 *Bq = Bbase + (int64_t)(q - td.q0) * T * LDF;
 #pragma unroll
             for (int i = 0; i < SL::BPT; ++i) {
