@@ -95,6 +95,23 @@ __device__ __forceinline__ float2 c2r_pre(float2 xk, float2 xp, float2 w) {
     const float2 o = cmul(d, conjf2(w));
     return make_float2(e.x - o.y, e.y + o.x);
 }
+// Both bins of a pair from one product: with W^{SH-k} = -conj W^k the (SH - k) output's
+// product is the conjugate of bin k's, so 2 X_{SH-k} = conj(sh) - i conj(W d) and
+// 2 (E + i O)_{SH-k} = conj(e) + i conj(o): 12 instructions per pair instead of 20.
+__device__ __forceinline__ void r2c_post_pair(float2 zk, float2 zp, float2 w, float2 &xk, float2 &xp) {
+    const float2 sh = make_float2(zk.x + zp.x, zk.y - zp.y);
+    const float2 d = make_float2(zk.x - zp.x, zk.y + zp.y);
+    const float2 wd = cmul(w, d);
+    xk = make_float2(sh.x + wd.y, sh.y - wd.x);
+    xp = make_float2(sh.x - wd.y, -sh.y - wd.x);
+}
+__device__ __forceinline__ void c2r_pre_pair(float2 xk, float2 xp, float2 w, float2 &zk, float2 &zp) {
+    const float2 e = make_float2(xk.x + xp.x, xk.y - xp.y);
+    const float2 d = make_float2(xk.x - xp.x, xk.y + xp.y);
+    const float2 o = cmul(d, conjf2(w));
+    zk = make_float2(e.x - o.y, e.y + o.x);
+    zp = make_float2(e.x + o.y, o.x - e.y);
+}
 
 // v * (SIGN < 0 ? -i : +i)
 template <int SIGN>
@@ -625,8 +642,7 @@ __global__ void __launch_bounds__(256, S == 512 ? 4 : S == 1024 ? 2 : 5) k_rows_
         for (int rr = rr0; rr < NB; rr += RPP, dst += RPP * LDF) {
             const float2 *wr = work + rr * RS;
             const float2 a = wr[k], b = wr[(SH - k) & (SH - 1)];
-            dst[k] = r2c_post(a, b, w);
-            dst[SH - k] = r2c_post(b, a, wc);
+            r2c_post_pair(a, b, w, dst[k], dst[SH - k]);
             if (k == 0) {
                 const float2 m = wr[HP];
                 dst[HP] = r2c_post(m, m, wm);
@@ -1433,12 +1449,12 @@ struct C2R {
             const float2 *sr = stg + rr * SS;
             float2 *wr = work + rr * RS;
             const float2 a = sr[k], b = sr[SH - k];
-            wr[k] = c2r_pre(a, b, w);
             if (k == 0) {
+                wr[0] = c2r_pre(a, b, w);
                 const float2 m = sr[HP];
                 wr[HP] = c2r_pre(m, m, wm);
             } else {
-                wr[SH - k] = c2r_pre(b, a, wc);
+                c2r_pre_pair(a, b, w, wr[k], wr[SH - k]);
             }
         }
     }
