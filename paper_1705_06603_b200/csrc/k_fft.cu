@@ -237,16 +237,36 @@ struct TwTable {
 // j = (tid / NB) * BPT + i.  Consecutive butterflies read and write adjacent
 // positions, so with an even STRIDE the exchanges move element pairs with 16-byte
 // shared-memory accesses (VEC): half the LDS/STS instructions of 8-byte accesses.
-template <int L, int NB, int STRIDE, int NTH, int s>
+//
+// MIR (the row passes at L = 256: 16 rows x 16 threads of 16 elements): the first and the
+// last stage give a thread the mirror butterflies j and 32 - j (j = 0 with 16) instead of
+// j, j + 1, so the positions n and L - n that the R2C post / C2R pre steps combine are both
+// in the thread's registers (no shared-memory pass for them).  Those two stages then move
+// single 8-byte elements; t = (tid & 7) | (tid >> 7) << 3 and m = (tid >> 3) & 15 keep
+// every access conflict-free (a half-warp = 8 rows x the butterflies of m, m + 1; a
+// quarter-warp = 8 rows at one position for the paired 16-byte accesses of the others).
+template <int L, int NB, int STRIDE, int NTH, int s, bool MIR = false>
 struct Stage {
-    static constexpr int R = fft_rad(L, s), Ns = fft_ns(L, s), LR = L / R;
+    static constexpr int R = fft_rad(L, s), Ns = fft_ns(L, s), LR = L / R, NS = fft_nst(L);
     static constexpr int E = NB * L / NTH, BPT = E / R;
     static_assert(E % R == 0, "elements per thread must be a multiple of the radix");
     static_assert(NTH * BPT * R == NB * L, "thread/butterfly mapping");
-    static constexpr bool VEC = (STRIDE % 2 == 0) && (BPT % 2 == 0) && (LR % 2 == 0);
+    static_assert(!MIR || (L == 256 && NB == 16 && NTH == 256 && NS == 3), "mirror mapping: 256-point rows");
+    static constexpr bool MS = MIR && (s == 0 || s == NS - 1);   // mirror butterflies in this stage
+    static_assert(!MS || (R == 8 && BPT == 2 && LR == 32), "mirror pairs j, 32 - j");
+    static constexpr bool VEC = (STRIDE % 2 == 0) && (BPT % 2 == 0) && (LR % 2 == 0) && !MS;
+    // outputs r, r + 1 of one first-stage butterfly are adjacent for any butterfly mapping
+    static constexpr bool VEC0 = (VEC || MS) && Ns == 1;
     __device__ static __forceinline__ void bj(int i, int tid, int &t, int &j) {
-        t = tid % NB;
-        j = (tid / NB) * BPT + i;
+        if constexpr (MIR) {
+            t = (tid & 7) | ((tid >> 7) << 3);
+            const int m = (tid >> 3) & 15;
+            if constexpr (MS) j = i == 0 ? m : (m == 0 ? 16 : 32 - m);
+            else j = m * BPT + i;
+        } else {
+            t = tid % NB;
+            j = (tid / NB) * BPT + i;
+        }
     }
     __device__ static __forceinline__ int in_n(int j, int r) { return j + r * LR; }
     __device__ static __forceinline__ int out_n(int j, int r) { return (j / Ns) * Ns * R + (j % Ns) + r * Ns; }
@@ -303,7 +323,7 @@ struct Stage {
         load_bfly_tw<SIGN>(buf, v, tid, TwTable{W, S});
     }
     __device__ static __forceinline__ void store(float2 *buf, const float2 (&v)[E], int tid) {
-        if constexpr (VEC && Ns == 1) {
+        if constexpr (VEC0) {
             // first stage: outputs r, r+1 of one butterfly are adjacent
 #pragma unroll
             for (int i = 0; i < BPT; ++i) {
@@ -343,46 +363,46 @@ struct Stage {
 // and last-stage outputs on exit.  Contains the barriers it needs.
 // TAIL = false drops the barrier after the last stage's loads, for callers whose next
 // write to `work` comes after a barrier of their own.
-template <int L, int NB, int STRIDE, int NTH, int SIGN, int s, int NS, bool TAIL = true>
+template <int L, int NB, int STRIDE, int NTH, int SIGN, int s, int NS, bool TAIL = true, bool MIR = false>
 struct Mid {
     static constexpr int E = NB * L / NTH;
     template <class TW>
     __device__ static __forceinline__ void run(float2 *work, float2 (&v)[E], int tid, const TW &tw) {
-        Stage<L, NB, STRIDE, NTH, s - 1>::store(work, v, tid);
+        Stage<L, NB, STRIDE, NTH, s - 1, MIR>::store(work, v, tid);
         // the stage's twiddles (a TMEM provider issues its loads here, under the barrier)
-        auto tws = tw.template pre<Stage<L, NB, STRIDE, NTH, s>::Ns>();
+        auto tws = tw.template pre<Stage<L, NB, STRIDE, NTH, s, MIR>::Ns>();
         __syncthreads();
         tws.ready();
-        Stage<L, NB, STRIDE, NTH, s>::template load_bfly_tw<SIGN>(work, v, tid, tws);
+        Stage<L, NB, STRIDE, NTH, s, MIR>::template load_bfly_tw<SIGN>(work, v, tid, tws);
         if (TAIL || s + 1 < NS) __syncthreads();
-        Mid<L, NB, STRIDE, NTH, SIGN, s + 1, NS, TAIL>::run(work, v, tid, tw);
+        Mid<L, NB, STRIDE, NTH, SIGN, s + 1, NS, TAIL, MIR>::run(work, v, tid, tw);
     }
 };
-template <int L, int NB, int STRIDE, int NTH, int SIGN, int NS, bool TAIL>
-struct Mid<L, NB, STRIDE, NTH, SIGN, NS, NS, TAIL> {
+template <int L, int NB, int STRIDE, int NTH, int SIGN, int NS, bool TAIL, bool MIR>
+struct Mid<L, NB, STRIDE, NTH, SIGN, NS, NS, TAIL, MIR> {
     static constexpr int E = NB * L / NTH;
     template <class TW>
     __device__ static __forceinline__ void run(float2 *, float2 (&)[E], int, const TW &) {}
 };
 
-template <int L, int NB, int STRIDE, int NTH>
+template <int L, int NB, int STRIDE, int NTH, bool MIR = false>
 struct Fft {
     static constexpr int NS = fft_nst(L);
     static constexpr int E = NB * L / NTH;
-    using First = Stage<L, NB, STRIDE, NTH, 0>;
-    using Last = Stage<L, NB, STRIDE, NTH, NS - 1>;
+    using First = Stage<L, NB, STRIDE, NTH, 0, MIR>;
+    using Last = Stage<L, NB, STRIDE, NTH, NS - 1, MIR>;
     template <int SIGN>
     __device__ static __forceinline__ void middle(float2 *work, float2 (&v)[E], int tid, const float2 *W, int S) {
-        Mid<L, NB, STRIDE, NTH, SIGN, 1, NS>::run(work, v, tid, TwTable{W, S});
+        Mid<L, NB, STRIDE, NTH, SIGN, 1, NS, true, MIR>::run(work, v, tid, TwTable{W, S});
     }
     template <int SIGN, class TW>
     __device__ static __forceinline__ void middle_tw(float2 *work, float2 (&v)[E], int tid, const TW &tw) {
-        Mid<L, NB, STRIDE, NTH, SIGN, 1, NS>::run(work, v, tid, tw);
+        Mid<L, NB, STRIDE, NTH, SIGN, 1, NS, true, MIR>::run(work, v, tid, tw);
     }
     // without the trailing barrier (the caller's next write to `work` follows a barrier)
     template <int SIGN, class TW>
     __device__ static __forceinline__ void middle_open(float2 *work, float2 (&v)[E], int tid, const TW &tw) {
-        Mid<L, NB, STRIDE, NTH, SIGN, 1, NS, false>::run(work, v, tid, tw);
+        Mid<L, NB, STRIDE, NTH, SIGN, 1, NS, false, MIR>::run(work, v, tid, tw);
     }
 };
 
@@ -393,8 +413,10 @@ struct GR {
     static constexpr int NTH = 256;
     static constexpr int NB = (S <= 64) ? 64 : (S <= 128) ? 32 : 16;
     static constexpr int RS = SH + 2;    // smem row stride (float2): even (16-byte pair exchanges), conflict-free
-    static constexpr int XS = S + 2;     // smem real-row stride (floats)
-    using F = Fft<SH, NB, RS, NTH>;
+    // smem real-row stride (floats): 4 banks per row for the mirror mapping's 8-byte accesses
+    static constexpr bool MIR = SH == 256 && NB == 16 && NTH == 256;
+    static constexpr int XS = S + (MIR ? 4 : 2);
+    using F = Fft<SH, NB, RS, NTH, MIR>;
     static constexpr int E = F::E;
 };
 // geometry of the column pass (length S complex transforms, NBC columns per CTA)
@@ -1437,6 +1459,39 @@ struct C2R {
         }
         __pipeline_commit();
     }
+    // mirror mapping: the stage-0 inputs straight from the staged spectrum rows, pre-processed
+    // in registers (the thread holds both members n, SH - n of each pair: butterflies j0 and
+    // j1 = 32 - j0, or 0 and 16), followed by the stage-0 butterflies -- no pass through work
+    __device__ static __forceinline__ void load_pre(const float2 *stg, float2 (&v)[G::E], const float2 *Wsm, int tid) {
+        using S0 = typename F::First;
+        static_assert(S0::MS && S0::R == 8 && S0::BPT == 2, "mirror first stage");
+        constexpr int HP = SH / 2;
+        int t, j0, j1;
+        S0::bj(0, tid, t, j0);
+        S0::bj(1, tid, t, j1);
+        const float2 *sr = stg + t * SS;
+        if (j0 != 0) {
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const int n = S0::in_n(j0, r);             // SH - n = in_n(j1, 7 - r)
+                c2r_pre_pair(sr[n], sr[SH - n], Wsm[n], v[r], v[8 + 7 - r]);
+            }
+        } else {
+            // j0 = 0: n = 32 r pairs with SH - n = 32 (8 - r); n = 0 with the Nyquist bin SH;
+            // n = SH / 2 with itself.  j1 = 16: n = 16 + 32 r with 16 + 32 (7 - r)
+            v[0] = c2r_pre(sr[0], sr[SH], Wsm[0]);
+#pragma unroll
+            for (int r = 1; r < 4; ++r) c2r_pre_pair(sr[32 * r], sr[SH - 32 * r], Wsm[32 * r], v[r], v[8 - r]);
+            v[4] = c2r_pre(sr[HP], sr[HP], Wsm[HP]);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int n = 16 + 32 * r;
+                c2r_pre_pair(sr[n], sr[SH - n], Wsm[n], v[8 + r], v[8 + 7 - r]);
+            }
+        }
+        S0::template bfly<+1>(&v[0], j0, Wsm, S);
+        S0::template bfly<+1>(&v[8], j1, Wsm, S);
+    }
     // half-length complex input z = E + i O from the staged spectrum rows -> work, one
     // (k, SH - k) pair per item; the self-paired k = SH/2 is done by the k = 0 item
     __device__ static __forceinline__ void pre(float2 *work, const float2 *stg, const float2 *Wsm, int tid) {
@@ -1530,11 +1585,17 @@ k_rows_inv(FftArgs A, int mode) {
     for (int qi = 0; qi < nq; ++qi) {
         __pipeline_wait_prior(0);
         __syncthreads();
-        C::pre(work, stg, Wsm, tid);
-        __syncthreads();
-        if (qi + 1 < nq) C::issue(stg, src(qi + 1), nrows, tid);   // in flight under this FFT
-        F::First::template load_bfly<+1>(work, v, tid, Wsm, S);
-        __syncthreads();
+        if constexpr (G::MIR) {
+            C::load_pre(stg, v, Wsm, tid);
+            __syncthreads();                                       // stg (= work for H) read
+            if (qi + 1 < nq) C::issue(stg, src(qi + 1), nrows, tid);
+        } else {
+            C::pre(work, stg, Wsm, tid);
+            __syncthreads();
+            if (qi + 1 < nq) C::issue(stg, src(qi + 1), nrows, tid);   // in flight under this FFT
+            F::First::template load_bfly<+1>(work, v, tid, Wsm, S);
+            __syncthreads();
+        }
         F::template middle<+1>(work, v, tid, Wsm, S);
         if constexpr (HT) {
             // g += wx_q . C2R(B_q): z[n] = (x[2n], x[2n+1]) at the last-stage positions
