@@ -188,11 +188,14 @@ __device__ __forceinline__ void dft8w(float2 *v, const float (&w)[8]) {
 // Radix plans.  For L >= 64 the first and the last stage are radix 8, so the
 // elements a thread produces in the last stage of one transform are exactly the
 // ones it consumes in the first stage of the next (accumulators stay in registers).
-__host__ __device__ constexpr int fft_nst(int L) {
-    return L == 16 ? 2 : L == 32 ? 2 : L == 64 ? 2 : L == 128 ? 3 : L == 256 ? 3 : L == 512 ? 3 : L == 1024 ? 4 : 0;
+// MAP = 2 (the forward row passes at L = 256): radix 16 x 16, one exchange per transform.
+__host__ __device__ constexpr int fft_nst(int L, int MAP = 0) {
+    return (MAP == 2 && L == 256) ? 2
+         : L == 16 ? 2 : L == 32 ? 2 : L == 64 ? 2 : L == 128 ? 3 : L == 256 ? 3 : L == 512 ? 3 : L == 1024 ? 4 : 0;
 }
-__host__ __device__ constexpr int fft_rad(int L, int s) {
-    return L == 16 ? 4
+__host__ __device__ constexpr int fft_rad(int L, int s, int MAP = 0) {
+    return (MAP == 2 && L == 256) ? 16
+         : L == 16 ? 4
          : L == 32 ? (s == 0 ? 8 : 4)
          : L == 64 ? 8
          : L == 128 ? (s == 1 ? 2 : 8)
@@ -200,7 +203,41 @@ __host__ __device__ constexpr int fft_rad(int L, int s) {
          : L == 512 ? 8
          : ((s == 1 || s == 2) ? 4 : 8);
 }
-__host__ __device__ constexpr int fft_ns(int L, int s) { return s == 0 ? 1 : fft_ns(L, s - 1) * fft_rad(L, s - 1); }
+__host__ __device__ constexpr int fft_ns(int L, int s, int MAP = 0) {
+    return s == 0 ? 1 : fft_ns(L, s - 1, MAP) * fft_rad(L, s - 1, MAP);
+}
+
+// X_k = sum_n a_n e^{SIGN 2 pi i n k / 16}: two radix-8 halves (even / odd n) and one
+// radix-2 combination with w16^k folded into FMAs
+template <int SIGN>
+__device__ __forceinline__ void dft16(float2 *v) {
+    float2 e[8], o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { e[k] = v[2 * k]; o[k] = v[2 * k + 1]; }
+    dft8<SIGN>(e[0], e[1], e[2], e[3], e[4], e[5], e[6], e[7]);
+    dft8<SIGN>(o[0], o[1], o[2], o[3], o[4], o[5], o[6], o[7]);
+    const float c1 = 0.92387953251128676f, s1 = 0.38268343236508977f, r = 0.70710678118654752f;
+    // w16^k = (cos 2 pi k / 16, SIGN sin 2 pi k / 16), k = 0..7
+    const float wr[8] = {1.f, c1, r, s1, 0.f, -s1, -r, -c1};
+    const float wi[8] = {0.f, SIGN * s1, SIGN * r, SIGN * c1, (float)SIGN, SIGN * c1, SIGN * r, SIGN * s1};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const float2 a = o[k], ek = e[k];
+        if (k == 0) {
+            v[0] = cadd(ek, a);
+            v[8] = csub(ek, a);
+        } else if (k == 4) {
+            const float2 t = rot90<SIGN>(a);
+            v[4] = cadd(ek, t);
+            v[12] = csub(ek, t);
+        } else {
+            v[k] = make_float2(__fmaf_rn(a.x, wr[k], __fmaf_rn(-a.y, wi[k], ek.x)),
+                               __fmaf_rn(a.x, wi[k], __fmaf_rn(a.y, wr[k], ek.y)));
+            v[k + 8] = make_float2(__fmaf_rn(-a.x, wr[k], __fmaf_rn(a.y, wi[k], ek.x)),
+                                   __fmaf_rn(-a.x, wi[k], __fmaf_rn(-a.y, wr[k], ek.y)));
+        }
+    }
+}
 
 // Twiddle providers for the stages with Ns > 1: get<Ns, R>(i, j, w) fills w[1..R-1] =
 // W_L^{r k}, k = j % Ns, for butterfly j (the thread's i-th of the stage).
@@ -228,6 +265,21 @@ struct TwTable {
             w[7] = cmul(w[4], w[3]);
         }
     }
+    // radix 16: w, w^2, w^4, w^8 from the table, the rest by at most three products
+    template <int Ns>
+    __device__ __forceinline__ void get16(int j, float2 (&w)[16]) const {
+        const int k = j % Ns;
+        const int step = S / (Ns * 16);
+        w[1] = W[(k * step) & (S - 1)];
+        w[2] = W[(2 * k * step) & (S - 1)];
+        w[4] = W[(4 * k * step) & (S - 1)];
+        w[8] = W[(8 * k * step) & (S - 1)];
+        w[3] = cmul(w[1], w[2]);
+#pragma unroll
+        for (int q = 5; q < 8; ++q) w[q] = cmul(w[4], w[q - 4]);
+#pragma unroll
+        for (int q = 9; q < 16; ++q) w[q] = cmul(w[8], w[q - 8]);
+    }
 };
 
 // One Stockham stage of NB batched length-L transforms at buf[t*STRIDE + n] executed
@@ -245,18 +297,21 @@ struct TwTable {
 // single 8-byte elements; t = (tid & 7) | (tid >> 7) << 3 and m = (tid >> 3) & 15 keep
 // every access conflict-free (a half-warp = 8 rows x the butterflies of m, m + 1; a
 // quarter-warp = 8 rows at one position for the paired 16-byte accesses of the others).
-template <int L, int NB, int STRIDE, int NTH, int s, bool MIR = false>
+// MAP = 2 (radix 16 x 16, one butterfly per thread per stage) uses the same t mapping with
+// j = m: 8-byte exchanges by 8 rows x 2 consecutive butterflies per half-warp.
+template <int L, int NB, int STRIDE, int NTH, int s, int MAP = 0>
 struct Stage {
-    static constexpr int R = fft_rad(L, s), Ns = fft_ns(L, s), LR = L / R, NS = fft_nst(L);
+    static constexpr bool MIR = MAP != 0;
+    static constexpr int R = fft_rad(L, s, MAP), Ns = fft_ns(L, s, MAP), LR = L / R, NS = fft_nst(L, MAP);
     static constexpr int E = NB * L / NTH, BPT = E / R;
     static_assert(E % R == 0, "elements per thread must be a multiple of the radix");
     static_assert(NTH * BPT * R == NB * L, "thread/butterfly mapping");
-    static_assert(!MIR || (L == 256 && NB == 16 && NTH == 256 && NS == 3), "mirror mapping: 256-point rows");
-    static constexpr bool MS = MIR && (s == 0 || s == NS - 1);   // mirror butterflies in this stage
+    static_assert(!MIR || (L == 256 && NB == 16 && NTH == 256), "row mappings: 256-point rows");
+    static constexpr bool MS = MAP == 1 && (s == 0 || s == NS - 1);   // mirror butterflies in this stage
     static_assert(!MS || (R == 8 && BPT == 2 && LR == 32), "mirror pairs j, 32 - j");
     static constexpr bool VEC = (STRIDE % 2 == 0) && (BPT % 2 == 0) && (LR % 2 == 0) && !MS;
     // outputs r, r + 1 of one first-stage butterfly are adjacent for any butterfly mapping
-    static constexpr bool VEC0 = (VEC || MS) && Ns == 1;
+    static constexpr bool VEC0 = (VEC || MIR) && Ns == 1 && STRIDE % 2 == 0 && R % 2 == 0;
     __device__ static __forceinline__ void bj(int i, int tid, int &t, int &j) {
         if constexpr (MIR) {
             t = (tid & 7) | ((tid >> 7) << 3);
@@ -272,6 +327,20 @@ struct Stage {
     __device__ static __forceinline__ int out_n(int j, int r) { return (j / Ns) * Ns * R + (j % Ns) + r * Ns; }
     template <int SIGN, class TW>
     __device__ static __forceinline__ void bfly_tw(float2 *v, int i, int j, const TW &tw) {
+        if constexpr (R == 16) {
+            if constexpr (Ns > 1) {
+                float2 w[16];
+                tw.template get16<Ns>(j, w);
+#pragma unroll
+                for (int r = 1; r < 16; ++r) {
+                    float2 ww = w[r];
+                    if (SIGN > 0) ww.y = -ww.y;
+                    v[r] = cmul(v[r], ww);
+                }
+            }
+            dft16<SIGN>(v);
+            return;
+        }
         if (Ns > 1) {
             float2 w[8];
             tw.template get<Ns, R>(i, j, w);
@@ -363,7 +432,7 @@ struct Stage {
 // and last-stage outputs on exit.  Contains the barriers it needs.
 // TAIL = false drops the barrier after the last stage's loads, for callers whose next
 // write to `work` comes after a barrier of their own.
-template <int L, int NB, int STRIDE, int NTH, int SIGN, int s, int NS, bool TAIL = true, bool MIR = false>
+template <int L, int NB, int STRIDE, int NTH, int SIGN, int s, int NS, bool TAIL = true, int MIR = 0>
 struct Mid {
     static constexpr int E = NB * L / NTH;
     template <class TW>
@@ -378,16 +447,16 @@ struct Mid {
         Mid<L, NB, STRIDE, NTH, SIGN, s + 1, NS, TAIL, MIR>::run(work, v, tid, tw);
     }
 };
-template <int L, int NB, int STRIDE, int NTH, int SIGN, int NS, bool TAIL, bool MIR>
+template <int L, int NB, int STRIDE, int NTH, int SIGN, int NS, bool TAIL, int MIR>
 struct Mid<L, NB, STRIDE, NTH, SIGN, NS, NS, TAIL, MIR> {
     static constexpr int E = NB * L / NTH;
     template <class TW>
     __device__ static __forceinline__ void run(float2 *, float2 (&)[E], int, const TW &) {}
 };
 
-template <int L, int NB, int STRIDE, int NTH, bool MIR = false>
+template <int L, int NB, int STRIDE, int NTH, int MIR = 0>
 struct Fft {
-    static constexpr int NS = fft_nst(L);
+    static constexpr int NS = fft_nst(L, MIR);
     static constexpr int E = NB * L / NTH;
     using First = Stage<L, NB, STRIDE, NTH, 0, MIR>;
     using Last = Stage<L, NB, STRIDE, NTH, NS - 1, MIR>;
@@ -416,7 +485,8 @@ struct GR {
     // smem real-row stride (floats): 4 banks per row for the mirror mapping's 8-byte accesses
     static constexpr bool MIR = SH == 256 && NB == 16 && NTH == 256;
     static constexpr int XS = S + (MIR ? 4 : 2);
-    using F = Fft<SH, NB, RS, NTH, MIR>;
+    using F = Fft<SH, NB, RS, NTH, MIR ? 1 : 0>;    // mirror ends (the C2R passes)
+    using FR = Fft<SH, NB, RS, NTH, MIR ? 2 : 0>;   // radix 16 x 16 (the R2C passes)
     static constexpr int E = F::E;
 };
 // geometry of the column pass (length S complex transforms, NBC columns per CTA)
@@ -482,7 +552,7 @@ template <int S, bool TMX>
 __global__ void __launch_bounds__(256, S == 512 ? 4 : S == 1024 ? 2 : 5) k_rows_fwd(FftArgs A, int mode, int par, const float *psfs, int npsf,
                                                   float2 *hrows) {
     using G = GR<S>;
-    using F = typename G::F;
+    using F = typename G::FR;
     constexpr int NB = G::NB, SH = G::SH, RS = G::RS, XS = G::XS, LDF = LD<S>::LDF;
     extern __shared__ __align__(16) float2 sm2[];
     float2 *Wsm = sm2;                                      // ROWS_TW(S) twiddles
