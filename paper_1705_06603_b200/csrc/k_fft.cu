@@ -1529,6 +1529,25 @@ struct C2R {
         }
         __pipeline_commit();
     }
+    // rows [0, nrows) of src0 -> stg by one bulk copy per row issued by thread 0 (SS * 8 =
+    // 2064 bytes: the SH + 1 bins and one pad element, a 16-byte multiple), completion counted
+    // on mbarrier m; rows >= nrows (the last row block of a tile) zero-filled by all threads.
+    // Replaces 2 k 16-byte cp.async per CTA (and their 64-bit address arithmetic).
+    __device__ static __forceinline__ void issue_bulk(float2 *stg, const float2 *src0, int nrows, int tid, uint64_t *m) {
+        constexpr uint32_t RB = SS * 8;
+        static_assert(SS == SH + 2 && RB % 16 == 0 && LDF >= SS, "bulk row copies");
+        if (tid == 0) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" :: "r"(smem_u32(m)), "r"(nrows * RB)
+                         : "memory");
+            for (int rr = 0; rr < nrows; ++rr)
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                             :: "r"(smem_u32(stg + rr * SS)), "l"(src0 + (int64_t)rr * LDF), "r"(RB), "r"(smem_u32(m))
+                             : "memory");
+        }
+        for (int idx = nrows * (SS / 2) + tid; idx < NB * (SS / 2); idx += G::NTH)
+            reinterpret_cast<float4 *>(stg)[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     // mirror mapping: the stage-0 inputs straight from the staged spectrum rows, pre-processed
     // in registers (the thread holds both members n, SH - n of each pair: butterflies j0 and
     // j1 = 32 - j0, or 0 and 16), followed by the stage-0 butterflies -- no pass through work
@@ -1631,8 +1650,16 @@ k_rows_inv(FftArgs A, int mode) {
             else
                 wxs[idx] = 0.f;
         }
+        if constexpr (G::MIR) __pipeline_commit();   // (the cp.async staging path commits them with its rows)
     }
-    if (nq > 0) C::issue(stg, src(0), nrows, tid);
+    __shared__ uint64_t sbar;                  // staging rows landed (bulk copies, mirror path)
+    uint32_t sphase = 0;
+    if constexpr (G::MIR) {
+        if (tid == 0) mbar_init(&sbar, 1);
+        if (nq > 0) C::issue_bulk(stg, src(0), nrows, tid, &sbar);
+    } else {
+        if (nq > 0) C::issue(stg, src(0), nrows, tid);
+    }
     for (int i = tid; i < ROWS_TW(S); i += G::NTH) Wsm[i] = A.W[i];
     float2 acc[(HT && !HTT) ? E : 1];
 #pragma unroll
@@ -1656,9 +1683,11 @@ k_rows_inv(FftArgs A, int mode) {
         __pipeline_wait_prior(0);
         __syncthreads();
         if constexpr (G::MIR) {
+            mbar_wait(&sbar, sphase);                              // the rows of this q landed
+            sphase ^= 1;
             C::load_pre(stg, v, Wsm, tid);
             __syncthreads();                                       // stg (= work for H) read
-            if (qi + 1 < nq) C::issue(stg, src(qi + 1), nrows, tid);
+            if (qi + 1 < nq) C::issue_bulk(stg, src(qi + 1), nrows, tid, &sbar);
         } else {
             C::pre(work, stg, Wsm, tid);
             __syncthreads();
