@@ -930,14 +930,23 @@ __global__ void __launch_bounds__(GC<S>::NTH) k_cols(FftArgs A, int mode, const 
                     for (int i = 0; i < S0::BPT; ++i) {
                         int t, j;
                         S0::bj(i, tid, t, j);
+                        float wv[8];
 #pragma unroll
                         for (int r = 0; r < S0::R; ++r) {
                             const int n = S0::in_n(j, r);
-                            const float2 c = colq[t * CS + n];
-                            const float wv = wys[n];
-                            v[i * S0::R + r] = make_float2(wv * c.x, wv * c.y);
+                            v[i * S0::R + r] = colq[t * CS + n];
+                            wv[r] = wys[n];
                         }
-                        S0::template bfly<-1>(&v[i * S0::R], j, Wsm, S);
+                        if constexpr (S0::R == 8 && S0::Ns == 1) {
+                            dft8w<-1>(&v[i * S0::R], wv);              // weights folded into the first level
+                        } else {
+#pragma unroll
+                            for (int r = 0; r < S0::R; ++r) {
+                                v[i * S0::R + r].x *= wv[r];
+                                v[i * S0::R + r].y *= wv[r];
+                            }
+                            S0::template bfly<-1>(&v[i * S0::R], j, Wsm, S);
+                        }
                     }
                 }
                 F::template middle<-1>(work, v, tid, Wsm, S);
@@ -963,7 +972,10 @@ __global__ void __launch_bounds__(GC<S>::NTH) k_cols(FftArgs A, int mode, const 
 #pragma unroll
                         for (int r = 0; r < SL::R; ++r) {
                             const float2 h = hbuf[hb_idx<NB>(SL::out_n(j, r), t)];
-                            acc[i * SL::R + r] = cadd(acc[i * SL::R + r], cmul(v[i * SL::R + r], h));
+                            const float2 x = v[i * SL::R + r];
+                            float2 &a = acc[i * SL::R + r];
+                            a.x = __fmaf_rn(x.x, h.x, __fmaf_rn(-x.y, h.y, a.x));
+                            a.y = __fmaf_rn(x.x, h.y, __fmaf_rn(x.y, h.x, a.y));
                         }
                     }
                 }
