@@ -492,8 +492,10 @@ struct GR {
 // geometry of the column pass (length S complex transforms, NBC columns per CTA)
 template <int S>
 struct GC {
-    // 256 threads, 8 columns per CTA from S = 256 up: ~104 KB smem at S = 512, two CTAs per SM
-    static constexpr int NTH = (S <= 128) ? 512 : 256;
+    // 8 columns per CTA from S = 256 up; at S = 256 (the strip plan) 128 threads of 16
+    // elements (paired 16-byte exchanges, 4 CTAs/SM), at S = 512 256 threads
+    static constexpr int NTH = (S <= 128) ? 512 : (S == 256) ? 128 : 256;
+    static constexpr int MINB = (S == 256 && NTH == 128) ? 4 : 1;
     static constexpr int NB = (S <= 64) ? 64 : (S <= 128) ? 32 : (S == 512) ? COLS_TM_NB : 8;
     static constexpr int CS = S + ((NB >= 16) ? 1 : 16 / NB);
     using F = Fft<S, NB, CS, NTH>;
@@ -813,7 +815,7 @@ __device__ __forceinline__ float2 hi2(float4 q) { return make_float2(q.z, q.w); 
 
 // mode 0: H; 1: H^T; 2: PSF spectra (forward column DFT of hrows -> Hhat)
 template <int S>
-__global__ void __launch_bounds__(GC<S>::NTH) k_cols(FftArgs A, int mode, const float2 *hrows, float2 *hhat, int npsf) {
+__global__ void __launch_bounds__(GC<S>::NTH, GC<S>::MINB) k_cols(FftArgs A, int mode, const float2 *hrows, float2 *hhat, int npsf) {
     using G = GC<S>;
     using F = typename G::F;
     constexpr int NB = G::NB, CS = G::CS, E = G::E, LDF = LD<S>::LDF, NF = S / 2 + 1, NTH = G::NTH;
