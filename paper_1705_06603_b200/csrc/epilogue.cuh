@@ -6,6 +6,7 @@ namespace deblur {
 
 constexpr int EPI_NT = 256;
 
+template <int NT = EPI_NT>
 __device__ __forceinline__ double block_sum(double v, double *scratch) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
@@ -14,7 +15,7 @@ __device__ __forceinline__ double block_sum(double v, double *scratch) {
     __syncthreads();
     double t = 0.0;
     if (threadIdx.x == 0)
-        for (int i = 0; i < EPI_NT / 32; ++i) t += scratch[i];
+        for (int i = 0; i < NT / 32; ++i) t += scratch[i];
     return t;
 }
 

@@ -479,7 +479,8 @@ struct Fft {
 template <int S>
 struct GR {
     static constexpr int SH = S / 2;
-    static constexpr int NTH = 256;
+    // 128 threads at S = 256 (the strip plan): 16 elements per thread, paired 16-byte exchanges
+    static constexpr int NTH = S == 256 ? 128 : 256;
     static constexpr int NB = (S <= 64) ? 64 : (S <= 128) ? 32 : 16;
     static constexpr int RS = SH + 2;    // smem row stride (float2): even (16-byte pair exchanges), conflict-free
     // smem real-row stride (floats): 4 banks per row for the mirror mapping's 8-byte accesses
@@ -551,7 +552,7 @@ __device__ __forceinline__ void tm_get(uint32_t ta, float2 (&v)[E]) {
 // TMX: the mode-0 instantiation with the TMEM stash (a kernel containing tcgen05 code ran
 // the other modes 2x slower, so they use the TMX = false instantiation)
 template <int S, bool TMX>
-__global__ void __launch_bounds__(256, S == 512 ? 4 : S == 1024 ? 2 : 5) k_rows_fwd(FftArgs A, int mode, int par, const float *psfs, int npsf,
+__global__ void __launch_bounds__(GR<S>::NTH, S == 512 ? 4 : S == 1024 ? 2 : GR<S>::NTH == 128 ? 6 : 5) k_rows_fwd(FftArgs A, int mode, int par, const float *psfs, int npsf,
                                                   float2 *hrows) {
     using G = GR<S>;
     using F = typename G::FR;
@@ -1619,7 +1620,7 @@ struct C2R {
 };
 
 template <int S, bool HT>
-__global__ void __launch_bounds__(256, S == 1024 ? (HT ? 1 : 2) : (HT && S == 512) ? 3 : 4)
+__global__ void __launch_bounds__(GR<S>::NTH, S == 1024 ? (HT ? 1 : 2) : (HT && S == 512) ? 3 : GR<S>::NTH == 128 ? 6 : 4)
 k_rows_inv(FftArgs A, int mode) {
     // H^T at S = 512: the accumulator sum_q wx_q C2R(B_q) lives in TMEM (32 columns per
     // thread) instead of 32 registers, so 3 CTAs/SM fit
@@ -1639,7 +1640,7 @@ k_rows_inv(FftArgs A, int mode) {
     float2 *stg = HT ? work + NB * RS : work;
     float *wxs = reinterpret_cast<float *>(stg + NB * C::SS);  // NQ x S (H^T)
     float *outs = reinterpret_cast<float *>(work);
-    __shared__ double red[256 / 32];
+    __shared__ double red[G::NTH / 32];
     const int tid = threadIdx.x;
     const int P = A.P, c2 = P - 1, T = S - P + 1;
     const int nblk = (T + NB - 1) / NB;
@@ -1878,7 +1879,7 @@ k_rows_inv(FftArgs A, int mode) {
         }
     }
     if (mode != FFT_PLAIN && A.partials) {
-        const double s = block_sum(dsum, red);
+        const double s = block_sum<G::NTH>(dsum, red);
         if (tid == 0) A.partials[blockIdx.x] = s;
     }
 }
