@@ -42,7 +42,7 @@
 #define ROWS_TW(S) ((S) / 2 + 2)
 #define COLS_TM_TW (S / 2)
 constexpr int COLS_TM_NB = 8;      // columns per CTA of the TMEM column pass (256 threads, 16 elements each)
-constexpr int COLS_TM_CPB = 3;     // column chunks per CTA (while the grid keeps >= 4 waves of 2 CTAs/SM)
+constexpr int COLS_TM_CPB = 4;     // column chunks per CTA (while the grid keeps >= 4 waves of 2 CTAs/SM)
 constexpr int COLS_TM_MINB = 2;    // CTAs per SM (128 registers, ~80 KB smem)
 
 
