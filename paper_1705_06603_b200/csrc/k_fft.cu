@@ -95,22 +95,23 @@ __device__ __forceinline__ float2 c2r_pre(float2 xk, float2 xp, float2 w) {
     const float2 o = cmul(d, conjf2(w));
     return make_float2(e.x - o.y, e.y + o.x);
 }
-// Both bins of a pair from one product: with W^{SH-k} = -conj W^k the (SH - k) output's
-// product is the conjugate of bin k's, so 2 X_{SH-k} = conj(sh) - i conj(W d) and
-// 2 (E + i O)_{SH-k} = conj(e) + i conj(o): 12 instructions per pair instead of 20.
-__device__ __forceinline__ void r2c_post_pair(float2 zk, float2 zp, float2 w, float2 &xk, float2 &xp) {
-    const float2 sh = make_float2(zk.x + zp.x, zk.y - zp.y);
-    const float2 d = make_float2(zk.x - zp.x, zk.y + zp.y);
-    const float2 wd = cmul(w, d);
-    xk = make_float2(sh.x + wd.y, sh.y - wd.x);
-    xp = make_float2(sh.x - wd.y, -sh.y - wd.x);
-}
+// Both bins of a C2R pre pair from one product: 2 (E + i O)_{SH-k} = conj(e) + i conj(o)
 __device__ __forceinline__ void c2r_pre_pair(float2 xk, float2 xp, float2 w, float2 &zk, float2 &zp) {
     const float2 e = make_float2(xk.x + xp.x, xk.y - xp.y);
     const float2 d = make_float2(xk.x - xp.x, xk.y + xp.y);
     const float2 o = cmul(d, conjf2(w));
     zk = make_float2(e.x - o.y, e.y + o.x);
     zp = make_float2(e.x + o.y, o.x - e.y);
+}
+// Both bins of an R2C post pair from one product: with W^{SH-k} = -conj W^k the (SH - k)
+// output's product is the conjugate of bin k's, so 2 X_{SH-k} = conj(sh) - i conj(W d)
+// (12 instructions per pair instead of 20).
+__device__ __forceinline__ void r2c_post_pair(float2 zk, float2 zp, float2 w, float2 &xk, float2 &xp) {
+    const float2 sh = make_float2(zk.x + zp.x, zk.y - zp.y);
+    const float2 d = make_float2(zk.x - zp.x, zk.y + zp.y);
+    const float2 wd = cmul(w, d);
+    xk = make_float2(sh.x + wd.y, sh.y - wd.x);
+    xp = make_float2(sh.x - wd.y, -sh.y - wd.x);
 }
 
 // v * (SIGN < 0 ? -i : +i)
@@ -290,15 +291,10 @@ struct TwTable {
 // positions, so with an even STRIDE the exchanges move element pairs with 16-byte
 // shared-memory accesses (VEC): half the LDS/STS instructions of 8-byte accesses.
 //
-// MIR (the row passes at L = 256: 16 rows x 16 threads of 16 elements): the first and the
-// last stage give a thread the mirror butterflies j and 32 - j (j = 0 with 16) instead of
-// j, j + 1, so the positions n and L - n that the R2C post / C2R pre steps combine are both
-// in the thread's registers (no shared-memory pass for them).  Those two stages then move
-// single 8-byte elements; t = (tid & 7) | (tid >> 7) << 3 and m = (tid >> 3) & 15 keep
-// every access conflict-free (a half-warp = 8 rows x the butterflies of m, m + 1; a
-// quarter-warp = 8 rows at one position for the paired 16-byte accesses of the others).
-// MAP = 2 (radix 16 x 16, one butterfly per thread per stage) uses the same t mapping with
-// j = m: 8-byte exchanges by 8 rows x 2 consecutive butterflies per half-warp.
+// MAP = 2 (the row passes at L = 256: 16 rows x 16 threads of 16 elements): radix 16 x 16,
+// one butterfly per thread per stage; t = (tid & 7) | (tid >> 7) << 3, j = (tid >> 3) & 15,
+// so a half-warp is 8 rows x 2 consecutive butterflies and the 8-byte exchanges are
+// conflict-free with the even row stride the paired 16-byte paths need.
 template <int L, int NB, int STRIDE, int NTH, int s, int MAP = 0>
 struct Stage {
     static constexpr bool MIR = MAP != 0;
@@ -306,18 +302,14 @@ struct Stage {
     static constexpr int E = NB * L / NTH, BPT = E / R;
     static_assert(E % R == 0, "elements per thread must be a multiple of the radix");
     static_assert(NTH * BPT * R == NB * L, "thread/butterfly mapping");
-    static_assert(!MIR || (L == 256 && NB == 16 && NTH == 256), "row mappings: 256-point rows");
-    static constexpr bool MS = MAP == 1 && (s == 0 || s == NS - 1);   // mirror butterflies in this stage
-    static_assert(!MS || (R == 8 && BPT == 2 && LR == 32), "mirror pairs j, 32 - j");
-    static constexpr bool VEC = (STRIDE % 2 == 0) && (BPT % 2 == 0) && (LR % 2 == 0) && !MS;
+    static_assert(!MIR || (MAP == 2 && L == 256 && NB == 16 && NTH == 256 && R == 16), "radix 16 x 16 rows");
+    static constexpr bool VEC = (STRIDE % 2 == 0) && (BPT % 2 == 0) && (LR % 2 == 0);
     // outputs r, r + 1 of one first-stage butterfly are adjacent for any butterfly mapping
     static constexpr bool VEC0 = (VEC || MIR) && Ns == 1 && STRIDE % 2 == 0 && R % 2 == 0;
     __device__ static __forceinline__ void bj(int i, int tid, int &t, int &j) {
         if constexpr (MIR) {
             t = (tid & 7) | ((tid >> 7) << 3);
-            const int m = (tid >> 3) & 15;
-            if constexpr (MS) j = i == 0 ? m : (m == 0 ? 16 : 32 - m);
-            else j = m * BPT + i;
+            j = ((tid >> 3) & 15) * BPT + i;
         } else {
             t = tid % NB;
             j = (tid / NB) * BPT + i;
@@ -483,11 +475,10 @@ struct GR {
     static constexpr int NTH = S == 256 ? 128 : 256;
     static constexpr int NB = (S <= 64) ? 64 : (S <= 128) ? 32 : 16;
     static constexpr int RS = SH + 2;    // smem row stride (float2): even (16-byte pair exchanges), conflict-free
-    // smem real-row stride (floats): 4 banks per row for the mirror mapping's 8-byte accesses
+    // smem real-row stride (floats): 4 banks per row for the row mapping's 8-byte accesses
     static constexpr bool MIR = SH == 256 && NB == 16 && NTH == 256;
     static constexpr int XS = S + (MIR ? 4 : 2);
-    using F = Fft<SH, NB, RS, NTH, MIR ? 1 : 0>;    // mirror ends (the C2R passes)
-    using FR = Fft<SH, NB, RS, NTH, MIR ? 2 : 0>;   // radix 16 x 16 (the R2C passes)
+    using F = Fft<SH, NB, RS, NTH, MIR ? 2 : 0>;    // radix 16 x 16 at S = 512
     static constexpr int E = F::E;
 };
 // geometry of the column pass (length S complex transforms, NBC columns per CTA)
@@ -555,7 +546,7 @@ template <int S, bool TMX>
 __global__ void __launch_bounds__(GR<S>::NTH, S == 512 ? 4 : S == 1024 ? 2 : GR<S>::NTH == 128 ? 6 : 5) k_rows_fwd(FftArgs A, int mode, int par, const float *psfs, int npsf,
                                                   float2 *hrows) {
     using G = GR<S>;
-    using F = typename G::FR;
+    using F = typename G::F;
     constexpr int NB = G::NB, SH = G::SH, RS = G::RS, XS = G::XS, LDF = LD<S>::LDF;
     extern __shared__ __align__(16) float2 sm2[];
     float2 *Wsm = sm2;                                      // ROWS_TW(S) twiddles
@@ -1563,38 +1554,22 @@ struct C2R {
         for (int idx = nrows * (SS / 2) + tid; idx < NB * (SS / 2); idx += G::NTH)
             reinterpret_cast<float4 *>(stg)[idx] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    // mirror mapping: the stage-0 inputs straight from the staged spectrum rows, pre-processed
-    // in registers (the thread holds both members n, SH - n of each pair: butterflies j0 and
-    // j1 = 32 - j0, or 0 and 16), followed by the stage-0 butterflies -- no pass through work
+    // radix 16 x 16 (S = 512): the stage-0 inputs straight from the staged spectrum rows,
+    // C2R-pre-processed in registers (each thread reads both members n, SH - n of its 16
+    // pairs and forms its own bins; no pass through the exchange buffer), then the stage-0
+    // butterfly
     __device__ static __forceinline__ void load_pre(const float2 *stg, float2 (&v)[G::E], const float2 *Wsm, int tid) {
         using S0 = typename F::First;
-        static_assert(S0::MS && S0::R == 8 && S0::BPT == 2, "mirror first stage");
-        constexpr int HP = SH / 2;
-        int t, j0, j1;
-        S0::bj(0, tid, t, j0);
-        S0::bj(1, tid, t, j1);
+        static_assert(S0::R == 16 && S0::BPT == 1, "radix-16 first stage");
+        int t, j;
+        S0::bj(0, tid, t, j);
         const float2 *sr = stg + t * SS;
-        if (j0 != 0) {
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                const int n = S0::in_n(j0, r);             // SH - n = in_n(j1, 7 - r)
-                c2r_pre_pair(sr[n], sr[SH - n], Wsm[n], v[r], v[8 + 7 - r]);
-            }
-        } else {
-            // j0 = 0: n = 32 r pairs with SH - n = 32 (8 - r); n = 0 with the Nyquist bin SH;
-            // n = SH / 2 with itself.  j1 = 16: n = 16 + 32 r with 16 + 32 (7 - r)
-            v[0] = c2r_pre(sr[0], sr[SH], Wsm[0]);
-#pragma unroll
-            for (int r = 1; r < 4; ++r) c2r_pre_pair(sr[32 * r], sr[SH - 32 * r], Wsm[32 * r], v[r], v[8 - r]);
-            v[4] = c2r_pre(sr[HP], sr[HP], Wsm[HP]);
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int n = 16 + 32 * r;
-                c2r_pre_pair(sr[n], sr[SH - n], Wsm[n], v[8 + r], v[8 + 7 - r]);
-            }
+        for (int r = 0; r < 16; ++r) {
+            const int n = S0::in_n(j, r);
+            v[r] = c2r_pre(sr[n], sr[SH - n], Wsm[n]);
         }
-        S0::template bfly<+1>(&v[0], j0, Wsm, S);
-        S0::template bfly<+1>(&v[8], j1, Wsm, S);
+        S0::template bfly<+1>(&v[0], j, Wsm, S);
     }
     // half-length complex input z = E + i O from the staged spectrum rows -> work, one
     // (k, SH - k) pair per item; the self-paired k = SH/2 is done by the k = 0 item
@@ -1667,7 +1642,7 @@ k_rows_inv(FftArgs A, int mode) {
         }
         if constexpr (G::MIR) __pipeline_commit();   // (the cp.async staging path commits them with its rows)
     }
-    __shared__ uint64_t sbar;                  // staging rows landed (bulk copies, mirror path)
+    __shared__ uint64_t sbar;                  // staging rows landed (bulk copies, S = 512)
     uint32_t sphase = 0;
     if constexpr (G::MIR) {
         if (tid == 0) mbar_init(&sbar, 1);
