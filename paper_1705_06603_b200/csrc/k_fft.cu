@@ -302,7 +302,7 @@ struct Stage {
     static constexpr int E = NB * L / NTH, BPT = E / R;
     static_assert(E % R == 0, "elements per thread must be a multiple of the radix");
     static_assert(NTH * BPT * R == NB * L, "thread/butterfly mapping");
-    static_assert(!MIR || (MAP == 2 && L == 256 && NB == 16 && NTH == 256 && R == 16), "radix 16 x 16 rows");
+    static_assert(!MIR || (MAP == 2 && L == 256 && NTH == 16 * NB && NB <= 16 && R == 16), "radix 16 x 16");
     static constexpr bool VEC = (STRIDE % 2 == 0) && (BPT % 2 == 0) && (LR % 2 == 0);
     // outputs r, r + 1 of one first-stage butterfly are adjacent for any butterfly mapping
     static constexpr bool VEC0 = (VEC || MIR) && Ns == 1 && STRIDE % 2 == 0 && R % 2 == 0;
@@ -490,7 +490,8 @@ struct GC {
     static constexpr int MINB = (S == 256 && NTH == 128) ? 4 : 1;
     static constexpr int NB = (S <= 64) ? 64 : (S <= 128) ? 32 : (S == 512) ? COLS_TM_NB : 8;
     static constexpr int CS = S + ((NB >= 16) ? 1 : 16 / NB);
-    using F = Fft<S, NB, CS, NTH>;
+    // S = 256: radix 16 x 16 (one exchange per transform), the row passes' thread mapping
+    using F = Fft<S, NB, CS, NTH, S == 256 ? 2 : 0>;
     static constexpr int E = F::E;
 };
 template <int S>
@@ -924,7 +925,7 @@ __global__ void __launch_bounds__(GC<S>::NTH, GC<S>::MINB) k_cols(FftArgs A, int
                     for (int i = 0; i < S0::BPT; ++i) {
                         int t, j;
                         S0::bj(i, tid, t, j);
-                        float wv[8];
+                        float wv[S0::R];
 #pragma unroll
                         for (int r = 0; r < S0::R; ++r) {
                             const int n = S0::in_n(j, r);
@@ -932,7 +933,8 @@ __global__ void __launch_bounds__(GC<S>::NTH, GC<S>::MINB) k_cols(FftArgs A, int
                             wv[r] = wys[n];
                         }
                         if constexpr (S0::R == 8 && S0::Ns == 1) {
-                            dft8w<-1>(&v[i * S0::R], wv);              // weights folded into the first level
+                            const float (&w8)[8] = reinterpret_cast<const float (&)[8]>(wv);
+                            dft8w<-1>(&v[i * S0::R], w8);              // weights folded into the first level
                         } else {
 #pragma unroll
                             for (int r = 0; r < S0::R; ++r) {
