@@ -191,11 +191,12 @@ __device__ __forceinline__ void dft8w(float2 *v, const float (&w)[8]) {
 // ones it consumes in the first stage of the next (accumulators stay in registers).
 // MAP = 2 (the forward row passes at L = 256): radix 16 x 16, one exchange per transform.
 __host__ __device__ constexpr int fft_nst(int L, int MAP = 0) {
-    return (MAP == 2 && L == 256) ? 2
+    return (MAP == 2 && (L == 256 || L == 128)) ? 2
          : L == 16 ? 2 : L == 32 ? 2 : L == 64 ? 2 : L == 128 ? 3 : L == 256 ? 3 : L == 512 ? 3 : L == 1024 ? 4 : 0;
 }
 __host__ __device__ constexpr int fft_rad(int L, int s, int MAP = 0) {
     return (MAP == 2 && L == 256) ? 16
+         : (MAP == 2 && L == 128) ? (s == 0 ? 16 : 8)
          : L == 16 ? 4
          : L == 32 ? (s == 0 ? 8 : 4)
          : L == 64 ? 8
@@ -302,14 +303,16 @@ struct Stage {
     static constexpr int E = NB * L / NTH, BPT = E / R;
     static_assert(E % R == 0, "elements per thread must be a multiple of the radix");
     static_assert(NTH * BPT * R == NB * L, "thread/butterfly mapping");
-    static_assert(!MIR || (MAP == 2 && L == 256 && NTH == 16 * NB && NB <= 16 && R == 16), "radix 16 x 16");
+    // MAP 2: 16 x L/16 (L = 256 or 128), L/16 threads per transform, 8 <= NB <= 16 transforms
+    static constexpr int TPR = L / 16, JB = TPR == 16 ? 4 : 3;
+    static_assert(!MIR || (MAP == 2 && (L == 256 || L == 128) && NTH == TPR * NB && NB >= 8 && NB <= 16), "radix 16 plans");
     static constexpr bool VEC = (STRIDE % 2 == 0) && (BPT % 2 == 0) && (LR % 2 == 0);
     // outputs r, r + 1 of one first-stage butterfly are adjacent for any butterfly mapping
     static constexpr bool VEC0 = (VEC || MIR) && Ns == 1 && STRIDE % 2 == 0 && R % 2 == 0;
     __device__ static __forceinline__ void bj(int i, int tid, int &t, int &j) {
         if constexpr (MIR) {
-            t = (tid & 7) | ((tid >> 7) << 3);
-            j = ((tid >> 3) & 15) * BPT + i;
+            t = (tid & 7) | ((tid >> (3 + JB)) << 3);
+            j = ((tid >> 3) & (TPR - 1)) * BPT + i;
         } else {
             t = tid % NB;
             j = (tid / NB) * BPT + i;
@@ -476,9 +479,10 @@ struct GR {
     static constexpr int NB = (S <= 64) ? 64 : (S <= 128) ? 32 : 16;
     static constexpr int RS = SH + 2;    // smem row stride (float2): even (16-byte pair exchanges), conflict-free
     // smem real-row stride (floats): 4 banks per row for the row mapping's 8-byte accesses
-    static constexpr bool MIR = SH == 256 && NB == 16 && NTH == 256;
+    // radix 16 x SH/16 with the row mapping at S = 512 (256 threads) and S = 256 (128)
+    static constexpr bool MIR = (SH == 256 || SH == 128) && NB == 16 && NTH == NB * SH / 16;
     static constexpr int XS = S + (MIR ? 4 : 2);
-    using F = Fft<SH, NB, RS, NTH, MIR ? 2 : 0>;    // radix 16 x 16 at S = 512
+    using F = Fft<SH, NB, RS, NTH, MIR ? 2 : 0>;
     static constexpr int E = F::E;
 };
 // geometry of the column pass (length S complex transforms, NBC columns per CTA)
@@ -1597,7 +1601,7 @@ struct C2R {
 };
 
 template <int S, bool HT>
-__global__ void __launch_bounds__(GR<S>::NTH, S == 1024 ? (HT ? 1 : 2) : (HT && S == 512) ? 3 : GR<S>::NTH == 128 ? 6 : 4)
+__global__ void __launch_bounds__(GR<S>::NTH, S == 1024 ? (HT ? 1 : 2) : (HT && S == 512) ? 3 : GR<S>::NTH == 128 ? (HT ? 5 : 6) : 4)
 k_rows_inv(FftArgs A, int mode) {
     // H^T at S = 512: the accumulator sum_q wx_q C2R(B_q) lives in TMEM (32 columns per
     // thread) instead of 32 registers, so 3 CTAs/SM fit
