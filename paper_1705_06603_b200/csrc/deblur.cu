@@ -689,7 +689,15 @@ deblur_status deblur_create(const deblur_params *p, deblur_t *out) {
     } while (0)
     CUC(cudaSetDevice(p->device));
     CUC(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-    CUC(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
+    {
+        // the exchange + consensus stream at the greatest priority: its few CTAs are
+        // dispatched ahead of the next iteration's H passes instead of trickling in beside
+        // them (c4: K5 0.144 ms instead of 1.13 ms spread over the H R2C pass; step time
+        // unchanged, 10.80 ms) -- the band values reach the neighbours as early as possible
+        int lo = 0, hi = 0;
+        CUC(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CUC(cudaStreamCreateWithPriority(&h->cstream, cudaStreamNonBlocking, hi));
+    }
     CUC(cudaEventCreateWithFlags(&h->ev_upd, cudaEventDisableTiming));
     CUC(cudaEventCreateWithFlags(&h->ev_cons, cudaEventDisableTiming));
     CUC(cudaStreamCreateWithFlags(&h->up_stream, cudaStreamNonBlocking));
