@@ -15,6 +15,7 @@ import pytest
 import synth
 from oracle import from_problem
 from paper_1705_06603_b200 import deblur as D
+from tests.fullsize import full_config
 
 pytestmark = pytest.mark.gpu
 
@@ -53,6 +54,30 @@ def test_loopback_bitwise_equal(k, n, facets, O, worlds, path, graphs, monkeypat
         np.testing.assert_array_equal(uv, u1)
         np.testing.assert_array_equal(ov, o1)
         np.testing.assert_array_equal(iv, i1)
+
+
+def test_loopback_c4_full_size_gpu_sweep():
+    """BASELINE's 1 -> 8 GPU sweep on c4 (16384^2, 4x2 facets) through the loopback transport,
+    in the launch configuration bench.py times (FFT path, graph replay): the facet states and
+    the objective after 3 iterations (both graph parities) are bitwise those of the
+    single-rank run for 2, 4 and 8 virtual ranks."""
+    pb = full_config(4)
+    ref = None
+    for V in (0, 2, 4, 8):
+        with D.Deblur.from_problem(pb, loopback_world=V) as dev:
+            assert dev.conv_path == D.CONV_FFT
+            dev.iterate(3)
+            x, u = dev.get_state()
+            obj = np.array(dev.objective())
+            n_x = dev.kernel_stats()["halo_exchange"][0]
+        if V == 0:
+            ref = (x, u, obj)
+            continue
+        assert n_x > 0
+        np.testing.assert_array_equal(x, ref[0])
+        np.testing.assert_array_equal(u, ref[1])
+        np.testing.assert_array_equal(obj, ref[2])
+        del x, u
 
 
 def test_loopback_vmlmb_and_traced():
