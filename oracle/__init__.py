@@ -13,10 +13,11 @@ Contents (each function cites the PAPER.md passage it follows):
   vmlmb.py                 VMLM-B Local-Solver (reading V1-V6) PAPER.md:287, :290
 
 Pins (tests/test_oracle_*.py, -m "not gpu") tie every function to something
-other than itself; see DESIGN.md §4 for the table.  "parity unpinned": the
-absolute iterate / objective values on the BASELINE configs are pinned only
-through the structural pins (single facet = centralized projected gradient,
-fixed point = consensus-reduced minimiser, exact-arithmetic trace).
+other than itself; see DESIGN.md §4 for the table.  No function here is
+"parity unpinned".  The paper prints no values for the BASELINE configs (their
+inputs are synthetic), so the absolute iterate / objective values there rest on
+the structural pins (single facet = centralized projected gradient, fixed
+point = consensus-reduced minimiser, exact-arithmetic trace).
 """
 from . import geometry, tv  # noqa: F401
 from .operators import Operator  # noqa: F401
