@@ -397,6 +397,11 @@ def args_config(pb):
 def run_reference(args, rank, world):
     if rank != 0:
         return
+    if world > 1 and "LOCAL_WORLD_SIZE" in os.environ:
+        # torchrun exports OMP_NUM_THREADS=1 to every rank; the other ranks have exited, so
+        # rank 0 runs the oracle on all host cores, as the N = 1 launch does (set before
+        # liboracle.so / libgomp is loaded)
+        os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
     pb = synth.make_config(args.config)
     n = min(pb.ny, args.ref_crop)
     d = oracle_sample(pb, n)

@@ -23,3 +23,20 @@ def test_reference_arm_json_line():
     assert d["config"]["workload"] == "c1"
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_reference_arm_under_torchrun():
+    """The driver's N > 1 launch of the reference arm: rank 0 alone runs the oracle (on all
+    host cores, not torchrun's OMP_NUM_THREADS=1) and prints the one line; the other rank
+    exits 0 without work."""
+    env = {k: v for k, v in os.environ.items() if k != "OMP_NUM_THREADS"}
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29731", os.path.join(ROOT, "bench.py"),
+                        "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0", "--ref-crop", "160",
+                        "--config", "1"], capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["cpu_baseline"]["cores"] == (os.cpu_count() or 1)
